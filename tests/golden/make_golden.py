@@ -1,0 +1,87 @@
+"""Regenerate tests/golden/golden.json from the UNMODIFIED reference.
+
+Runs oracle/_ref/refjoin (the reference library compiled from
+/root/reference/proj/src by oracle/Makefile) and records:
+  * join:  canonical-row digest (oracle.cpp:77-88 + BASELINE.md §2 formula),
+           emission-order digest, output rows and clusteredness for every
+           variant over the acceptance criterion-1 grid
+           (tests/acceptance_main.cpp:63-79, r_pay=2, s_pay=1) plus C1, the
+           mixed-width C3 shape and duplicate-build (--swap) cells;
+  * gen:   column digests of workloads::gen_pk_fk outputs;
+  * prim:  primitive known-answer digests (refjoin.cpp cmd_prim).
+Only runs where /root/reference exists (this container); the JSON is committed.
+
+    python tests/golden/make_golden.py
+"""
+import json
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+from oracle import oracle as O  # noqa: E402
+
+
+def grid():
+    cells, seed = [], 1
+    for rows in (1024, 16384):
+        for match in (0.0, 0.25, 0.5, 1.0):
+            for zipf in (0.0, 1.0, 2.0):
+                for key in ("u32", "u64"):
+                    cells.append(dict(r=rows, s=2 * rows, match=match, zipf=zipf, key=key,
+                                      pay=key, rpay=2, spay=1, seed=seed))
+                    seed += 1
+    return cells
+
+
+def wl_args(c):
+    a = ["--r", str(c["r"]), "--s", str(c["s"]), "--rpay", str(c["rpay"]), "--spay",
+         str(c["spay"]), "--key", c["key"], "--pay", c["pay"], "--match", str(c["match"]),
+         "--zipf", str(c["zipf"]), "--seed", str(c["seed"])]
+    if c.get("widths"):
+        a += ["--widths", c["widths"]]
+    if c.get("swap"):
+        a += ["--swap"]
+    return a
+
+
+def main():
+    O.build()
+    out = {"join": [], "gen": [], "prim": {}}
+    cells = grid()
+    cells.append(dict(r=1 << 20, s=1 << 22, match=1.0, zipf=0.0, key="u32", pay="u32", rpay=1,
+                      spay=1, seed=42, name="C1"))
+    cells.append(dict(r=4096, s=8192, match=0.5, zipf=0.0, key="u64", pay="u64", rpay=4, spay=4,
+                      seed=42, widths="4,8,4,8", name="C3-shape"))
+    for z in (0.5, 1.0, 1.5):
+        cells.append(dict(r=8192, s=16384, match=1.0, zipf=z, key="u32", pay="u32", rpay=2,
+                          spay=2, seed=42, name=f"C4-shape-z{z}"))
+    for seed, z in ((101, 1.0), (102, 2.0)):
+        cells.append(dict(r=2048, s=4096, match=1.0, zipf=z, key="u32", pay="u32", rpay=1,
+                          spay=2, seed=seed, swap=True, name=f"dup-build-z{z}"))
+    for c in cells:
+        for algo in ("phj", "smj"):
+            for pat in ("gftr", "gfur"):
+                r = O.refjoin("join", *wl_args(c), "--algo", algo, "--pattern", pat, "--digest",
+                              "--threads", "4")
+                out["join"].append(dict(cell=c, algo=algo, pattern=pat, rows_out=r["rows_out"],
+                                        digest=r["digest"], order_digest=r["order_digest"],
+                                        clusteredness_r=r["clusteredness_r"],
+                                        clusteredness_s=r["clusteredness_s"]))
+        print(c, file=sys.stderr)
+    for c in (cells[0], cells[5], cells[-7], cells[-6], cells[-3]):
+        out["gen"].append(dict(cell=c, digests=O.refjoin("gen", *wl_args(c))))
+    c2 = dict(r=1 << 27, s=1 << 28, match=1.0, zipf=0.0, key="u32", pay="u32", rpay=2, spay=2,
+              seed=42, name="C2")
+    if os.environ.get("GOLDEN_C2"):
+        out["gen"].append(dict(cell=c2, digests=O.refjoin("gen", *wl_args(c2))))
+    for n, seed in ((5000, 2), (100000, 1)):
+        out["prim"][f"{n}:{seed}"] = O.refjoin("prim", "--n", str(n), "--seed", str(seed))
+    with open(os.path.join(HERE, "golden.json"), "w") as f:
+        json.dump(out, f, indent=1, sort_keys=True)
+
+
+if __name__ == "__main__":
+    main()
