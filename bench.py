@@ -1,0 +1,372 @@
+#!/usr/bin/env python
+"""bench.py — end-to-end equi-join throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one run_join of the headline workload (BASELINE.json configs[1],
+"C2"): PK-FK |R| = 2^27, |S| = 2^28, 4-byte key + 2 x 4-byte payload columns
+per relation, uniform foreign keys, match ratio 1, GFTR partitioned hash join
+(PHJ-OM).  Inputs are bit-identical to the reference's workloads::gen_pk_fk
+(seed 42), generated on the device.  value = (|R|+|S|) / step time with inputs
+resident in HBM (transform + find + materialise, the reference's PhaseReport
+scope, mem_ledger.hpp:231-246); e2e = the same through the host-buffer C-ABI
+(cj_run_join_host) with pinned host inputs and outputs, copies included.
+
+Under torchrun (N>1) every rank joins its own C2-sized shard (weak scaling);
+the step time is the max over ranks.  --impl reference times the reference's
+own CPU engine (oracle/_ref/refjoin, compiled from the reference sources) on
+the host cores, on rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "end-to-end join throughput (|R|+|S| tuples/s incl. materialisation) vs HBM roofline"
+R_ROWS, S_ROWS, NPAY, SEED = 1 << 27, 1 << 28, 2, 42
+WORKLOAD = ("C2: PK-FK |R|=2^27, |S|=2^28, 4-byte key + 2 x 4-byte payloads per relation, "
+            "uniform FKs, match ratio 1, seed 42")
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--variant", default="phj-gftr")
+    p.add_argument("--scale-log2", type=int, default=0,
+                   help="shrink |R|,|S| by 2^k (debug only; the headline uses 0)")
+    p.add_argument("--no-extras", action="store_true", help="skip variants/e2e/cpu legs")
+    return p.parse_args()
+
+
+def b_alg(algo: str, pattern: str, nr: int, ns: int, nt: int, k=4, w=(4, 4)) -> float:
+    """Algorithmic bytes of one join: PHJ P=2 passes, SMJ P=4
+    live 8-bit digits (keys < 2^28), tuple ids 4 B; gathers count 4 + 2w per
+    output element."""
+    P = 2 if algo == "phj" else 4
+    if pattern == "gftr":
+        t = sum(k * n + P * 2 * (k + w[0]) * n for n in (nr, ns))
+        f = k * (nr + ns) + (k + 8) * nt
+        m = 0
+        for n in (nr, ns):
+            m += (4 + 2 * w[0]) * nt
+            for wc in w[1:]:
+                m += P * 2 * (k + wc) * n + (4 + 2 * wc) * nt
+    else:
+        t = sum(k * n + P * 2 * (k + 4) * n for n in (nr, ns))
+        f = k * (nr + ns) + (k + 16) * nt
+        m = 2 * sum((4 + 2 * wc) * nt for wc in w)
+    return float(t + f + m)
+
+
+def b_min(nr, ns, nt, k=4, w=(4, 4)):
+    return float((k + sum(w)) * (nr + ns) + (k + 2 * sum(w)) * nt)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap,power.draw")
+
+    def __init__(self, gpu: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        rows = [r.split(", ") for r in self.f.read().strip().splitlines() if r.strip()]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4)
+                          if len(r) > 2 + i and r[2 + i].strip() == "Active"})
+        busy = [x for x in sm if x > 600] or sm
+        return {"sm_mhz": statistics.median(busy) if busy else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def reference_arm(a):
+    """Reference CPU engine on the host cores (rank 0 only), same config."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    if not O.refjoin_available():
+        print(json.dumps({"impl": "reference",
+                          "unavailable": "oracle/_ref/refjoin not built (needs /root/reference)"}))
+        return
+    algo, pattern = a.variant.split("-")
+    nr, ns = R_ROWS >> a.scale_log2, S_ROWS >> a.scale_log2
+    cores = os.cpu_count() or 1
+    env = dict(os.environ, OMP_NUM_THREADS=str(cores))
+    r = O.refjoin("join", "--r", str(nr), "--s", str(ns), "--rpay", str(NPAY), "--spay", str(NPAY),
+                  "--seed", str(SEED), "--algo", algo, "--pattern", pattern, "--prealloc",
+                  "--threads", str(cores), "--reps", str(a.steps), "--warmup", str(a.warmup),
+                  env=env)
+    ms = r["total_ns_mean"] / 1e6
+    v = (nr + ns) / (ms / 1e3)
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "tuples/s", "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic (gen_pk_fk, seed 42)",
+        "config": {"workload": WORKLOAD, "variant": a.variant.upper(), "r_rows": nr, "s_rows": ns},
+        "cpu_baseline": {"value": v, "unit": "tuples/s", "cores": cores, "kind": "reference",
+                         "sample": f"full workload, {a.steps} timed run_join calls "
+                                   f"(preallocate=true, {cores} OpenMP threads)"},
+        "e2e": {"value": v, "unit": "tuples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "phases_ms": {"transform": r["transform_ns"] / 1e6, "find": r["find_ns"] / 1e6,
+                      "materialize": r["materialize_ns"] / 1e6},
+    }))
+
+
+def cpu_baseline(nr, ns, variant):
+    """oracle/_ref (the reference compiled from its sources) on this host."""
+    from oracle import oracle as O
+    if not O.refjoin_available():
+        return None
+    algo, pattern = variant.split("-")
+    cores = os.cpu_count() or 1
+    # bounded sample: 1/4 of the workload (same shape), one timed call
+    snr, sns = nr >> 2, ns >> 2
+    try:
+        r = O.refjoin("join", "--r", str(snr), "--s", str(sns), "--rpay", str(NPAY), "--spay",
+                      str(NPAY), "--seed", str(SEED), "--algo", algo, "--pattern", pattern,
+                      "--prealloc", "--threads", str(cores), "--reps", "1",
+                      env=dict(os.environ, OMP_NUM_THREADS=str(cores)), timeout=600)
+    except Exception as e:  # noqa: BLE001
+        return {"value": None, "unit": "tuples/s", "cores": cores, "kind": "reference",
+                "sample": f"failed: {e}"}
+    v = (snr + sns) / (r["total_ns_mean"] / 1e9)
+    return {"value": v, "unit": "tuples/s", "cores": cores, "kind": "reference",
+            "sample": f"|R|=2^{snr.bit_length()-1}, |S|=2^{sns.bit_length()-1} (1/4 of the "
+                      f"workload, same shape), one run_join, {cores} threads, preallocate=true",
+            "ms": r["total_ns_mean"] / 1e6}
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return reference_arm(a)
+    import torch
+    import torch.distributed as dist
+    import paper_2312_00720_b200 as cj
+    from paper_2312_00720_b200 import _capi as A
+    import ctypes as C
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx = cj.Context(local)
+    algo, pattern = a.variant.split("-")
+    nr, ns = R_ROWS >> a.scale_log2, S_ROWS >> a.scale_log2
+    R, S = cj.gen_pk_fk(ctx, nr, ns, NPAY, NPAY, 4, 4, 1.0, 0.0, SEED + rank)
+    Rc, Sc = cj.coljoin.c_relation(R), cj.coljoin.c_relation(S)
+    opt = cj.options(algo, pattern)
+    res = A.JoinResult()
+    L = A.lib()
+
+    def step():
+        A.check(L.cj_run_join(ctx.h, C.byref(Rc), C.byref(Sc), C.byref(opt), C.byref(res)),
+                ctx.h, "run_join")
+        rows = res.rows
+        phases = (res.transform_ns, res.find_ns, res.materialize_ns)
+        A.check(L.cj_result_free(ctx.h, C.byref(res)), ctx.h, "free")
+        return rows, phases
+
+    for _ in range(a.warmup):
+        rows, _ = step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = Clocks(local)
+    A.check(L.cj_set_kernel_timing(ctx.h, 1), ctx.h, "timing")
+    l0 = ctx.launches
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record(ctx.stream)
+    phase_sum = [0, 0, 0]
+    for _ in range(a.steps):
+        rows, ph = step()
+        for i in range(3):
+            phase_sum[i] += ph[i]
+    ev1.record(ctx.stream)
+    torch.cuda.synchronize()
+    launches = ctx.launches - l0
+    ms = ev0.elapsed_time(ev1) / a.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+        ms = float(t.item())
+    clk = clocks.stop()
+    # per-kernel records of the timed region
+    names = (C.c_char_p * 4096)()
+    kms = (C.c_float * 4096)()
+    kby = (C.c_uint64 * 4096)()
+    cnt = C.c_int()
+    A.check(L.cj_kernel_records(ctx.h, 4096, names, kms, kby, C.byref(cnt)), ctx.h, "records")
+    A.check(L.cj_set_kernel_timing(ctx.h, 0), ctx.h, "timing")
+    agg = {}
+    for i in range(min(cnt.value, 4096)):
+        n = names[i].decode()
+        e = agg.setdefault(n, [0, 0.0, 0])
+        e[0] += 1
+        e[1] += kms[i]
+        e[2] += kby[i]
+    peak, peak_src = peaks()
+    kernels = sorted(({"kernel": n, "launches": c, "ms_per_step": t / a.steps,
+                       "share": t / (ms * a.steps) if ms else None,
+                       "alg_gbs": (b / 1e9) / (t / 1e3) if t else None}
+                      for n, (c, t, b) in agg.items()), key=lambda d: -d["ms_per_step"])
+    dom = kernels[0] if kernels else None
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(dom["kernel"]) if dom else None
+    except Exception:
+        pass
+    roofline = None
+    if dom:
+        c, t, b = agg[dom["kernel"]]
+        achieved = (b / c) / 1e9 / ((t / c) / 1e3)
+        roofline = {"bound": "hbm", "kernel": dom["kernel"], "achieved": achieved, "peak": peak,
+                    "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                    "alg_bytes_per_launch": b / c, "peak_source": peak_src}
+    tuples = (nr + ns) * world
+    value = tuples / (ms / 1e3)
+    balg = b_alg(algo, pattern, nr, ns, rows)
+    out = {
+        "metric": METRIC, "value": value, "unit": "tuples/s", "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic: bit-identical to the reference's workloads::gen_pk_fk "
+                "(seed 42 + rank), generated on the device",
+        "config": {"workload": WORKLOAD if a.scale_log2 == 0 else f"C2/2^{a.scale_log2}",
+                   "variant": a.variant.upper(), "r_rows": nr, "s_rows": ns, "out_rows": rows,
+                   "l2": "inputs 4.5 GiB >> 126 MB L2 (no flush needed)",
+                   "parallelism": f"radix-sharded x{world}" if world > 1 else "single GPU"},
+        "roofline": roofline,
+        "join_roofline": {"b_alg_bytes": balg, "b_min_bytes": b_min(nr, ns, rows),
+                          "frac_b_alg": balg / (ms / 1e3) / (peak * 1e9),
+                          "frac_b_min": b_min(nr, ns, rows) / (ms / 1e3) / (peak * 1e9)},
+        "phases_ms": {"transform": phase_sum[0] / 1e6 / a.steps,
+                      "find_and_fused_materialize": phase_sum[1] / 1e6 / a.steps,
+                      "materialize": phase_sum[2] / 1e6 / a.steps},
+        "gpu_launches": launches, "clocks": clk, "kernels": kernels,
+    }
+    if rank == 0 and world == 1 and not a.no_extras:
+        # the other variants (3 timed steps each)
+        var = {}
+        for v in ("phj-gftr", "smj-gftr", "phj-gfur", "smj-gfur", "nphj-gftr", "nphj-gfur"):
+            o = cj.options(*v.split("-"))
+            step_opt = o
+
+            def vstep():
+                A.check(L.cj_run_join(ctx.h, C.byref(Rc), C.byref(Sc), C.byref(step_opt),
+                                      C.byref(res)), ctx.h, "run_join")
+                A.check(L.cj_result_free(ctx.h, C.byref(res)), ctx.h, "free")
+            vstep()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(ctx.stream)
+            for _ in range(3):
+                vstep()
+            e1.record(ctx.stream)
+            torch.cuda.synchronize()
+            vms = e0.elapsed_time(e1) / 3
+            va, vp = v.split("-")
+            var[v] = {"ms": vms, "tuples_per_s": (nr + ns) / (vms / 1e3),
+                      "frac_b_alg": (b_alg(va, vp, nr, ns, rows) / (vms / 1e3) / (peak * 1e9)
+                                     if va != "nphj" else None)}
+        out["variants"] = var
+        # end to end through the host-buffer C-ABI (pinned host in/out)
+        out["e2e"] = e2e_leg(ctx, R, S, opt, steps=3)
+        out["cpu_baseline"] = cpu_baseline(nr, ns, a.variant)
+    if rank == 0:
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e_leg(ctx, R, S, opt, steps=3):
+    import ctypes as C
+    import torch
+    from paper_2312_00720_b200 import _capi as A
+    import paper_2312_00720_b200 as cj
+    L = A.lib()
+    hk = [R.key.cpu().pin_memory()] + [p.cpu().pin_memory() for p in R.payloads]
+    sk = [S.key.cpu().pin_memory()] + [p.cpu().pin_memory() for p in S.payloads]
+    Rh = cj.Relation(hk[0], hk[1:], "R", True)
+    Sh = cj.Relation(sk[0], sk[1:], "S", False)
+    Rc, Sc = cj.coljoin.c_relation(Rh), cj.coljoin.c_relation(Sh)  # data_ptr() of pinned host
+    out_bytes = S.key.numel() * (4 + 4 * (len(R.payloads) + len(S.payloads)))
+    arena = torch.empty(out_bytes + 4096 * 8, dtype=torch.uint8).pin_memory()
+    base = arena.data_ptr()
+    state = {"off": 0}
+
+    def alloc(nbytes, _user):
+        p = base + state["off"]
+        state["off"] += (int(nbytes) + 255) & ~255
+        return p
+
+    cb = A.HOST_ALLOC(alloc)
+    res = A.JoinResult()
+    h2d, d2h = C.c_uint64(), C.c_uint64()
+    times = []
+    for i in range(steps + 1):
+        state["off"] = 0
+        t0 = time.perf_counter()
+        A.check(L.cj_run_join_host(ctx.h, C.byref(Rc), C.byref(Sc), C.byref(opt), cb, None,
+                                   C.byref(res), C.byref(h2d), C.byref(d2h)), ctx.h, "e2e")
+        t1 = time.perf_counter()
+        if i:
+            times.append(t1 - t0)
+    t = statistics.mean(times)
+    n = R.key.numel() + S.key.numel()
+    bi = sum(x.numel() * x.element_size() for x in hk + sk)
+    bo = res.rows * (4 + 4 * (len(R.payloads) + len(S.payloads)))
+    return {"value": n / t, "unit": "tuples/s", "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo,
+            "ms_per_step": t * 1e3, "h2d_ms": h2d.value / 1e6, "d2h_ms": d2h.value / 1e6,
+            "api": "cj_run_join_host (pinned host columns in, pinned host columns out)",
+            "steps": steps}
+
+
+if __name__ == "__main__":
+    main()

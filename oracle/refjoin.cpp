@@ -4,7 +4,7 @@
 // golden fixtures under tests/golden/.
 //
 //   refjoin join  [workload opts] --algo phj|smj --pattern gftr|gfur
-//                 [--reps N] [--threads T] [--prealloc] [--digest] [--dump DIR]
+//                 [--reps N] [--warmup W] [--threads T] [--prealloc] [--digest] [--dump DIR]
 //   refjoin prim  --n N --seed S [--dump DIR]
 //   refjoin gen   [workload opts] --dump DIR
 //   (--swap builds on S, whose keys repeat, and probes with R)
@@ -150,12 +150,17 @@ int cmd_join(const Args& a) {
   task.options.preallocate = a.has("--prealloc");
   task.options.total_radix_bits = std::atoi(a.get("--total-bits", "-1"));
   const int reps = std::max(1, std::atoi(a.get("--reps", "1")));
+  const int warmup = std::max(0, std::atoi(a.get("--warmup", "0")));
   std::vector<uint64_t> totals;
   JoinOutput out;
+  for (int i = 0; i < warmup; ++i) out = run_join(task);
   for (int i = 0; i < reps; ++i) {
     out = run_join(task);
     totals.push_back(out.report.total_ns());
   }
+  uint64_t sum = 0;
+  for (uint64_t t : totals) sum += t;
+  const uint64_t mean = sum / totals.size();
   std::sort(totals.begin(), totals.end());
   const uint64_t med = totals[totals.size() / 2];
   const double tput = static_cast<double>(r.rows() + s.rows()) / (med * 1e-9);
@@ -183,12 +188,12 @@ int cmd_join(const Args& a) {
                                                      : static_cast<unsigned>(omp_get_max_threads());
   std::printf(
       "{\"variant\": \"%s\", \"rows_r\": %zu, \"rows_s\": %zu, \"rows_out\": %zu, "
-      "\"threads\": %u, \"reps\": %d, \"total_ns_median\": %llu, \"transform_ns\": %llu, "
+      "\"threads\": %u, \"reps\": %d, \"total_ns_mean\": %llu, \"total_ns_median\": %llu, \"transform_ns\": %llu, "
       "\"find_ns\": %llu, \"materialize_ns\": %llu, \"tuples_per_s\": %.6e, "
       "\"clusteredness_r\": %.6f, \"clusteredness_s\": %.6f, \"digest\": %s, "
       "\"order_digest\": %s}\n",
       variant_name(task.algorithm, task.pattern), r.rows(), s.rows(), out.relation.rows(),
-      threads, reps, (unsigned long long)med, (unsigned long long)out.report.transform_ns,
+      threads, reps, (unsigned long long)mean, (unsigned long long)med, (unsigned long long)out.report.transform_ns,
       (unsigned long long)out.report.find_ns, (unsigned long long)out.report.materialize_ns,
       tput, out.stats.clusteredness_r, out.stats.clusteredness_s, dig.c_str(), odig.c_str());
   return 0;

@@ -1,0 +1,176 @@
+// Internal declarations shared by the .cu translation units of
+// libcoljoin_b200.so.  Not part of the public boundary (include/cj_api.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "cj_api.h"
+
+namespace cj {
+
+constexpr int kRadix = 256;  // digits per pass (<= 8 bits, primitives.cpp:15)
+
+// A status error carrying a cj_status; converted at the C boundary.
+struct Error {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg);
+void check_cuda(cudaError_t e, const char* what);
+#define CJ_CUDA(x) ::cj::check_cuda((x), #x)
+
+}  // namespace cj
+
+struct cj_ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  uint16_t epoch = 0;             // look-back status generation (see radix.cu)
+  uint64_t launches = 0;          // kernels launched through this ctx
+  std::string last_error;
+  // persistent scratch (grown on demand, never shrunk)
+  uint64_t* status = nullptr;     // decoupled look-back words
+  uint64_t status_words = 0;
+  uint32_t* counters = nullptr;   // tile / unit tickets, error word
+  uint32_t* err_word = nullptr;   // device error flags (OOB, overflow)
+  uint32_t* host_pinned = nullptr;// small pinned staging (4 KiB)
+  cudaEvent_t marks[16] = {};
+  // per-launch timing records (cj_set_kernel_timing): event pairs around each
+  // kernel on the ctx stream, with the launch's algorithmic bytes
+  struct KernelRec {
+    const char* name;
+    cudaEvent_t a, b;
+    uint64_t bytes;
+  };
+  bool timing = false;
+  std::vector<KernelRec> recs;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  cudaEvent_t take_event();
+  void kbegin(const char* name, uint64_t alg_bytes);  // before a launch
+  void kend();                                       // after it
+  void set_bytes(const char* name, uint64_t bytes);  // fix up the last record of `name`
+
+  void* alloc(uint64_t bytes);
+  void release(void* p);
+  uint16_t next_epoch();          // fresh look-back generation (memsets on wrap)
+  uint64_t* status_buffer(uint64_t words);
+  uint32_t* ticket(int slot);     // zeroed device counter (slot < 64)
+};
+
+namespace cj {
+
+// Scoped device scratch released on the ctx stream at scope exit.
+struct Scratch {
+  cj_ctx* ctx;
+  void* p = nullptr;
+  Scratch(cj_ctx* c, uint64_t bytes) : ctx(c), p(c->alloc(bytes ? bytes : 16)) {}
+  ~Scratch() { if (p) ctx->release(p); }
+  Scratch(const Scratch&) = delete;
+  Scratch& operator=(const Scratch&) = delete;
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+// ---- radix.cu ---------------------------------------------------------------
+struct ValCols {
+  int n = 0;
+  const void* in[CJ_MAX_COLS + 1] = {};
+  void* out[CJ_MAX_COLS + 1] = {};
+  uint32_t bytes[CJ_MAX_COLS + 1] = {};
+  int gen_ids = 0;   // column 0 generated as the source index (u32)
+};
+
+struct PassPlan {
+  int npasses = 0;
+  uint32_t lo[64] = {}, hi[64] = {};
+};
+
+// Digit counts of every pass in one read of the keys; counts_dev[p*256 + d].
+// Also writes the exclusive digit bases base_dev[p*256+d] (u64) and returns
+// which passes are live (not constant) after one host round trip.
+void histogram_passes(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes,
+                      const PassPlan& plan, uint32_t* counts_dev, uint64_t* base_dev,
+                      std::vector<uint32_t>* counts_host);
+
+// One stable scatter pass (onesweep; decoupled look-back across tiles).
+void scatter_pass(cj_ctx* ctx, const void* keys_in, void* keys_out, uint64_t n, int key_bytes,
+                  uint32_t lo, uint32_t hi, const uint64_t* base_dev, const ValCols& vals);
+
+// Stable LSD over the plan; constant-digit passes skipped; the last executed
+// pass lands in the caller's outputs.  gen_ids handled in the first pass.
+void lsd_partition(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, int key_bytes,
+                   const PassPlan& plan, const ValCols& vals,
+                   std::vector<uint32_t>* counts_host = nullptr);
+
+// Layout offsets (fanout + 1) of keys sorted by their low `bits`: binary search
+// of every boundary.
+void partition_offsets(cj_ctx* ctx, const void* keys_sorted, uint64_t n, int key_bytes,
+                       uint32_t bits, uint64_t* offsets_dev);
+
+void copy_columns(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, int key_bytes,
+                  const ValCols& vals);
+
+// ---- gather.cu ----------------------------------------------------------------
+void gather_cols(cj_ctx* ctx, const void* const* in, uint64_t n_in, const uint32_t* map,
+                 uint64_t m, void* const* out, const uint32_t* bytes, int ncols);
+
+// ---- join kernels ---------------------------------------------------------------
+struct OutSpec {
+  void* key = nullptr;             // K[]
+  uint32_t* ids_r = nullptr;       // u32[]
+  uint32_t* ids_s = nullptr;
+  const uint32_t* carried_r = nullptr;  // physical ids: ids_r = carried_r[i]
+  const uint32_t* carried_s = nullptr;
+  int nr = 0, ns = 0;              // fused payload columns per side
+  const void* r_src[CJ_MAX_COLS] = {};
+  const void* s_src[CJ_MAX_COLS] = {};
+  void* r_dst[CJ_MAX_COLS] = {};
+  void* s_dst[CJ_MAX_COLS] = {};
+  uint32_t r_bytes[CJ_MAX_COLS] = {};
+  uint32_t s_bytes[CJ_MAX_COLS] = {};
+};
+
+// hash_join.cu: partitioned hash join (count + look-back + fill), outputs per
+// OutSpec; capacity = rows the outputs can hold (CJ_ERR_CAPACITY_EXCEEDED
+// beyond).  Returns the match count (one host sync).
+uint64_t phj_find(cj_ctx* ctx, const void* bkeys, const uint64_t* boff, const void* pkeys,
+                  const uint64_t* poff, uint32_t fanout, int key_bytes, uint32_t limit,
+                  const OutSpec& out, uint64_t capacity);
+// Match count only (for sizing outputs), plus optional per-reference-unit counts.
+uint64_t phj_count(cj_ctx* ctx, const void* bkeys, const uint64_t* boff, const void* pkeys,
+                   const uint64_t* poff, uint32_t fanout, int key_bytes, uint32_t limit);
+
+// merge_join.cu: merge join over sorted keys; same contract.
+uint64_t smj_find(cj_ctx* ctx, const void* rkeys, uint64_t nr, const void* skeys, uint64_t ns,
+                  int key_bytes, bool pk_fk, const OutSpec& out, uint64_t capacity);
+uint64_t smj_count(cj_ctx* ctx, const void* rkeys, uint64_t nr, const void* skeys, uint64_t ns,
+                   int key_bytes, bool pk_fk);
+void check_sorted(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes, bool strict,
+                  int err_code, const char* what);
+
+// nphj.cu: non-partitioned (global table) hash join.
+uint64_t nphj_find(cj_ctx* ctx, const void* rkeys, uint64_t nr, const void* skeys, uint64_t ns,
+                   int key_bytes, const OutSpec& out, uint64_t capacity, bool count_only);
+
+// gen.cu
+void gen_pk_fk(cj_ctx* ctx, uint64_t r_rows, uint64_t s_rows, uint32_t r_pay, uint32_t s_pay,
+               uint32_t key_bytes, uint32_t pay_bytes, double match_ratio, double zipf,
+               uint64_t seed, void* r_key, void* const* r_pays, void* s_key, void* const* s_pays);
+
+// error word helpers: kernels OR codes into ctx->err_word; raise after sync
+enum : uint32_t { kErrOOB = 1u, kErrOverflow = 2u, kErrNotSorted = 4u, kErrDupKeys = 8u };
+void raise_device_errors(cj_ctx* ctx);
+
+inline unsigned grid_for(uint64_t work, unsigned per_block, unsigned cap) {
+  uint64_t g = (work + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  return static_cast<unsigned>(g > cap ? cap : g);
+}
+
+}  // namespace cj

@@ -1,0 +1,933 @@
+// Context, error plumbing, the run_join device pipeline and the C-ABI
+// (include/cj_api.h).
+//
+// Reference: run_join (join_engine.cpp:255-361), transform_side (:68-113),
+// materialize_gfur (:161-176), materialize_gftr (:180-253).
+//
+// Pipelines (B200 design, all device-resident):
+//   PHJ-GFTR  transform: key + ALL payload columns of a side partitioned in one
+//             LSD pass sequence (the reference re-partitions payloads 2..n on
+//             demand, join_engine.cpp:180-213; carrying them in the same scatter
+//             reads the key once per pass and skips the re-transforms).
+//             find+materialise: one fused kernel writes finished output rows,
+//             gathering R payloads from the staged build chunk and S payloads
+//             at the (clustered) probe positions.
+//   SMJ-GFTR  transform: full-width stable sort of key + all payloads;
+//             find+materialise: fused merge-join kernel.
+//   *-GFUR    transform: (key, id) with ids born in pass 1; find writes
+//             physical ids (SMJ resolves them in the same kernel); materialise
+//             gathers every payload from the untransformed relations.
+//   NPHJ      global-table hash join (no partitioning), see nphj.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "cj_device.cuh"
+#include "cj_internal.cuh"
+
+namespace cj {
+
+void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+
+void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    const int code = e == cudaErrorMemoryAllocation ? CJ_ERR_OUT_OF_MEMORY : CJ_ERR_CUDA;
+    fail(code, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+void raise_device_errors(cj_ctx* ctx) {
+  CJ_CUDA(cudaMemcpyAsync(ctx->host_pinned + 64, ctx->err_word, sizeof(uint32_t),
+                          cudaMemcpyDeviceToHost, ctx->stream));
+  CJ_CUDA(cudaStreamSynchronize(ctx->stream));
+  const uint32_t e = ctx->host_pinned[64];
+  if (!e) return;
+  CJ_CUDA(cudaMemsetAsync(ctx->err_word, 0, sizeof(uint32_t), ctx->stream));
+  CJ_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (e & kErrOOB) fail(CJ_ERR_INDEX_OUT_OF_BOUNDS, "gather map entry past input length");
+  if (e & kErrOverflow) fail(CJ_ERR_CAPACITY_EXCEEDED, "join output exceeds its capacity");
+  if (e & kErrNotSorted) fail(CJ_ERR_NOT_SORTED, "keys not ascending");
+  if (e & kErrDupKeys) fail(CJ_ERR_DUPLICATE_BUILD_KEYS, "pk-fk mode requires unique build keys");
+  if (e & dev::kErrStall) fail(CJ_ERR_CUDA, "decoupled look-back stalled (internal error)");
+}
+
+namespace {
+
+__global__ void k_abs_diff_sum(const uint32_t* __restrict__ ids, uint64_t n,
+                               unsigned long long* out) {
+  uint64_t acc = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x + 1; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t a = ids[i - 1], b = ids[i];
+    acc += a > b ? a - b : b - a;
+  }
+  acc = dev::warp_sum(acc);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, (unsigned long long)acc);
+}
+
+// primitives.cpp:398-407 gather_clusteredness over a device map
+double clusteredness(cj_ctx* ctx, const uint32_t* ids, uint64_t n) {
+  if (n <= 1) return 1.0;
+  Scratch acc(ctx, 8);
+  CJ_CUDA(cudaMemsetAsync(acc.p, 0, 8, ctx->stream));
+  ctx->kbegin("clusteredness", n * 4);
+  k_abs_diff_sum<<<grid_for(n, 256 * 16, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+      ids, n, acc.as<unsigned long long>());
+  ctx->kend();
+  uint64_t* h = reinterpret_cast<uint64_t*>(ctx->host_pinned);
+  CJ_CUDA(cudaMemcpyAsync(h, acc.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CJ_CUDA(cudaStreamSynchronize(ctx->stream));
+  return static_cast<double>(h[0]) / static_cast<double>(n - 1);
+}
+
+unsigned default_total_radix_bits(uint64_t build_rows) {  // task.hpp:45-50
+  if (build_rows > (1ull << 20)) return 16;
+  unsigned bits = 0;
+  while ((build_rows >> bits) > 1024) ++bits;
+  return bits > 16 ? 16 : bits;
+}
+
+PassPlan plan_bits(unsigned total_bits, unsigned per_pass) {  // task.hpp:54-63
+  if (per_pass == 0 || per_pass > 8) fail(CJ_ERR_FANOUT_TOO_LARGE, "bits per pass must be in [1, 8]");
+  PassPlan p;
+  for (unsigned lo = 0; lo < total_bits; lo += per_pass) {
+    if (p.npasses == CJ_MAX_PASSES * 3) break;
+    p.lo[p.npasses] = lo;
+    p.hi[p.npasses] = std::min(lo + per_pass, total_bits);
+    ++p.npasses;
+  }
+  return p;
+}
+
+PassPlan full_width_plan(int key_bytes) { return plan_bits((unsigned)key_bytes * 8, 8); }
+
+void check_key_bytes(uint32_t kb) {
+  if (kb != 4 && kb != 8) fail(CJ_ERR_KIND, "key must be a 4- or 8-byte integer column");
+}
+
+// LSD plans longer than CJ_MAX_PASSES (e.g. 20 bits at 1 bit/pass) run in
+// segments; each segment is itself stable, so the composition is the plan.
+void lsd_any(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, int kb,
+             const PassPlan& plan, const ValCols& vals) {
+  if (plan.npasses <= CJ_MAX_PASSES) {
+    lsd_partition(ctx, keys, keys_out, n, kb, plan, vals);
+    return;
+  }
+  const void* cur = keys;
+  ValCols v = vals;
+  for (int s = 0; s < plan.npasses; s += CJ_MAX_PASSES) {
+    PassPlan seg;
+    seg.npasses = std::min(CJ_MAX_PASSES, plan.npasses - s);
+    for (int i = 0; i < seg.npasses; ++i) {
+      seg.lo[i] = plan.lo[s + i];
+      seg.hi[i] = plan.hi[s + i];
+    }
+    lsd_partition(ctx, cur, keys_out, n, kb, seg, v);
+    cur = keys_out;
+    for (int c = 0; c < v.n; ++c) v.in[c] = v.out[c];
+    v.gen_ids = 0;
+  }
+}
+
+struct Side {
+  void* keys = nullptr;
+  void* cols[CJ_MAX_COLS + 1] = {};   // transformed carried columns
+  uint64_t* offsets = nullptr;        // PHJ layout (device)
+};
+
+struct Timer {
+  cj_ctx* ctx;
+  cudaEvent_t ev[4];
+  explicit Timer(cj_ctx* c) : ctx(c) {
+    for (auto& e : ev) CJ_CUDA(cudaEventCreate(&e));
+  }
+  ~Timer() {
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
+  void mark(int i) { CJ_CUDA(cudaEventRecord(ev[i], ctx->stream)); }
+  uint64_t ns(int a, int b) {
+    float ms = 0;
+    CJ_CUDA(cudaEventElapsedTime(&ms, ev[a], ev[b]));
+    return static_cast<uint64_t>(ms * 1e6);
+  }
+};
+
+void validate_relation(const cj_relation* r, const char* what) {
+  if (!r) fail(CJ_ERR_SPEC_INVALID, std::string("join task needs ") + what);
+  check_key_bytes(r->key_bytes);
+  if (r->rows > 0x7fffffffull) fail(CJ_ERR_SPEC_INVALID, "relation exceeds the 2^31-1 row cap");
+  if (r->npay > CJ_MAX_COLS) fail(CJ_ERR_UNSUPPORTED, "too many payload columns");
+  for (uint32_t c = 0; c < r->npay; ++c)
+    if (r->pay_bytes[c] != 4 && r->pay_bytes[c] != 8)
+      fail(CJ_ERR_KIND, "payload columns must be 4- or 8-byte integers");
+}
+
+// Transform one side: partition (PHJ) or sort (SMJ) the key with the carried
+// columns.  gfur: carried = generated ids; gftr: carried = every payload.
+Side transform(cj_ctx* ctx, const cj_relation* rel, int algo, bool gfur, unsigned total_bits,
+               unsigned bits_per_pass, std::vector<void*>& owned) {
+  Side s;
+  const uint64_t n = rel->rows;
+  const int kb = (int)rel->key_bytes;
+  s.keys = ctx->alloc(std::max<uint64_t>(n * kb, 16));
+  owned.push_back(s.keys);
+  ValCols v;
+  if (gfur) {
+    v.n = 1;
+    v.gen_ids = 1;
+    v.in[0] = nullptr;
+    v.bytes[0] = 4;
+    v.out[0] = ctx->alloc(std::max<uint64_t>(n * 4, 16));
+    owned.push_back(v.out[0]);
+  } else {
+    v.n = (int)rel->npay;
+    for (uint32_t c = 0; c < rel->npay; ++c) {
+      v.in[c] = rel->pay[c];
+      v.bytes[c] = rel->pay_bytes[c];
+      v.out[c] = ctx->alloc(std::max<uint64_t>(n * rel->pay_bytes[c], 16));
+      owned.push_back(v.out[c]);
+    }
+  }
+  for (int c = 0; c < v.n; ++c) s.cols[c] = v.out[c];
+  if (algo == CJ_SMJ) {
+    lsd_any(ctx, rel->key, s.keys, n, kb, full_width_plan(kb), v);
+  } else {
+    s.offsets = static_cast<uint64_t*>(ctx->alloc(sizeof(uint64_t) * ((1ull << total_bits) + 1)));
+    owned.push_back(s.offsets);
+    if (total_bits == 0) {
+      copy_columns(ctx, rel->key, s.keys, n, kb, v);
+    } else {
+      lsd_any(ctx, rel->key, s.keys, n, kb, plan_bits(total_bits, bits_per_pass), v);
+    }
+    partition_offsets(ctx, s.keys, n, kb, total_bits, s.offsets);
+  }
+  return s;
+}
+
+void alloc_output(cj_ctx* ctx, const cj_relation* r, const cj_relation* s, uint64_t cap,
+                  bool ids, cj_join_result* res) {
+  const uint64_t c = std::max<uint64_t>(cap, 1);
+  res->key = ctx->alloc(c * r->key_bytes);
+  for (uint32_t i = 0; i < r->npay; ++i) res->pay[i] = ctx->alloc(c * r->pay_bytes[i]);
+  for (uint32_t i = 0; i < s->npay; ++i) res->pay[r->npay + i] = ctx->alloc(c * s->pay_bytes[i]);
+  if (ids) {
+    res->ids_r = static_cast<uint32_t*>(ctx->alloc(c * 4));
+    res->ids_s = static_cast<uint32_t*>(ctx->alloc(c * 4));
+  }
+}
+
+void free_output(cj_ctx* ctx, cj_join_result* res) {
+  if (res->key) ctx->release(res->key);
+  res->key = nullptr;
+  for (auto& p : res->pay) {
+    if (p) ctx->release(p);
+    p = nullptr;
+  }
+  if (res->ids_r) ctx->release(res->ids_r);
+  if (res->ids_s) ctx->release(res->ids_s);
+  res->ids_r = res->ids_s = nullptr;
+}
+
+void run_join_dev(cj_ctx* ctx, const cj_relation* R, const cj_relation* S,
+                  const cj_join_options* opt, cj_join_result* res) {
+  validate_relation(R, "a build relation");
+  validate_relation(S, "a probe relation");
+  if (R->key_bytes != S->key_bytes) fail(CJ_ERR_KIND, "build and probe key kinds differ");
+  if (opt->radix_bits_per_pass == 0 || opt->radix_bits_per_pass > 8)
+    fail(CJ_ERR_FANOUT_TOO_LARGE, "radix bits per pass must be in [1, 8]");
+  if (opt->algo != CJ_SMJ && opt->algo != CJ_PHJ && opt->algo != CJ_NPHJ)
+    fail(CJ_ERR_SPEC_INVALID, "unknown join algorithm");
+  const int kb = (int)R->key_bytes;
+  const bool gfur = opt->pattern == CJ_GFUR;
+  const bool pk_fk = R->key_unique != 0;
+  const unsigned total_bits = opt->total_radix_bits >= 0 ? (unsigned)opt->total_radix_bits
+                                                         : default_total_radix_bits(R->rows);
+  if (opt->algo == CJ_PHJ && (total_bits > 20 || total_bits > (unsigned)kb * 8))
+    fail(CJ_ERR_FANOUT_TOO_LARGE, "partition fan-out capped at 2^20 and the key width");
+  const bool want_ids = opt->want_ids || opt->want_stats;
+  std::memset(res, 0, sizeof(*res));
+  std::vector<void*> owned;
+  Timer tm(ctx);
+  struct Guard {
+    cj_ctx* ctx;
+    std::vector<void*>* v;
+    ~Guard() {
+      for (void* p : *v) ctx->release(p);
+    }
+  } guard{ctx, &owned};
+
+  if (opt->algo == CJ_NPHJ) {
+    // No transform: the build relation is hashed as is (nphj.cu).
+    tm.mark(0);
+    tm.mark(1);
+    OutSpec o;
+    uint64_t cap = pk_fk ? S->rows : nphj_find(ctx, R->key, R->rows, S->key, S->rows, kb, o, 0, true);
+    alloc_output(ctx, R, S, cap, true, res);
+    o.key = res->key;
+    o.ids_r = res->ids_r;
+    o.ids_s = res->ids_s;
+    if (!gfur) {  // GFTR: payload rows carried in the table / probe order
+      o.nr = (int)R->npay;
+      o.ns = (int)S->npay;
+      for (uint32_t c = 0; c < R->npay; ++c) {
+        o.r_src[c] = R->pay[c];
+        o.r_dst[c] = res->pay[c];
+        o.r_bytes[c] = R->pay_bytes[c];
+      }
+      for (uint32_t c = 0; c < S->npay; ++c) {
+        o.s_src[c] = S->pay[c];
+        o.s_dst[c] = res->pay[R->npay + c];
+        o.s_bytes[c] = S->pay_bytes[c];
+      }
+    }
+    uint64_t total;
+    try {
+      total = nphj_find(ctx, R->key, R->rows, S->key, S->rows, kb, o, cap, false);
+    } catch (const Error& e) {
+      if (e.code != CJ_ERR_CAPACITY_EXCEEDED || !pk_fk) throw;
+      free_output(ctx, res);
+      OutSpec oc;
+      cap = nphj_find(ctx, R->key, R->rows, S->key, S->rows, kb, oc, 0, true);
+      alloc_output(ctx, R, S, cap, true, res);
+      o.key = res->key;
+      o.ids_r = res->ids_r;
+      o.ids_s = res->ids_s;
+      for (uint32_t c = 0; c < R->npay && !gfur; ++c) o.r_dst[c] = res->pay[c];
+      for (uint32_t c = 0; c < S->npay && !gfur; ++c) o.s_dst[c] = res->pay[R->npay + c];
+      total = nphj_find(ctx, R->key, R->rows, S->key, S->rows, kb, o, cap, false);
+    }
+    tm.mark(2);
+    if (gfur) {
+      const void* in[2 * CJ_MAX_COLS];
+      void* out[2 * CJ_MAX_COLS];
+      uint32_t by[2 * CJ_MAX_COLS];
+      for (uint32_t c = 0; c < R->npay; ++c) {
+        in[c] = R->pay[c];
+        out[c] = res->pay[c];
+        by[c] = R->pay_bytes[c];
+      }
+      gather_cols(ctx, in, R->rows, res->ids_r, total, out, by, (int)R->npay);
+      for (uint32_t c = 0; c < S->npay; ++c) {
+        in[c] = S->pay[c];
+        out[c] = res->pay[R->npay + c];
+        by[c] = S->pay_bytes[c];
+      }
+      gather_cols(ctx, in, S->rows, res->ids_s, total, out, by, (int)S->npay);
+    }
+    tm.mark(3);
+    CJ_CUDA(cudaStreamSynchronize(ctx->stream));
+    raise_device_errors(ctx);
+    res->rows = total;
+    res->transform_ns = tm.ns(0, 1);
+    res->find_ns = tm.ns(1, 2);
+    res->materialize_ns = tm.ns(2, 3);
+    if (opt->want_stats) {
+      res->clusteredness_r = clusteredness(ctx, res->ids_r, total);
+      res->clusteredness_s = clusteredness(ctx, res->ids_s, total);
+    }
+    if (!want_ids) {
+      ctx->release(res->ids_r);
+      ctx->release(res->ids_s);
+      res->ids_r = res->ids_s = nullptr;
+    }
+    return;
+  }
+
+  // ---- transform ----------------------------------------------------------
+  tm.mark(0);
+  Side tr = transform(ctx, R, opt->algo, gfur, total_bits, opt->radix_bits_per_pass, owned);
+  Side ts = transform(ctx, S, opt->algo, gfur, total_bits, opt->radix_bits_per_pass, owned);
+  tm.mark(1);
+
+  // ---- find (+ fused materialise for GFTR) ------------------------------------
+  if (opt->algo == CJ_SMJ && opt->validate) {
+    check_sorted(ctx, tr.keys, R->rows, kb, false, CJ_ERR_NOT_SORTED, "build");
+    check_sorted(ctx, ts.keys, S->rows, kb, false, CJ_ERR_NOT_SORTED, "probe");
+    if (pk_fk) check_sorted(ctx, tr.keys, R->rows, kb, true, CJ_ERR_DUPLICATE_BUILD_KEYS, "pk");
+  }
+  const uint32_t fanout = 1u << total_bits;
+  auto count = [&]() -> uint64_t {
+    if (opt->algo == CJ_SMJ) return smj_count(ctx, tr.keys, R->rows, ts.keys, S->rows, kb, pk_fk);
+    return phj_count(ctx, tr.keys, tr.offsets, ts.keys, ts.offsets, fanout, kb,
+                     opt->sub_partition_limit);
+  };
+  // PK-FK: at most one match per probe row (sized without a count pass); a
+  // mislabelled build with duplicates overflows and is re-run exactly.
+  uint64_t cap = pk_fk ? S->rows : count();
+  auto find = [&](uint64_t capacity) -> uint64_t {
+    OutSpec o;
+    o.key = res->key;
+    o.ids_r = res->ids_r;
+    o.ids_s = res->ids_s;
+    if (gfur) {
+      o.ids_r = res->ids_r ? res->ids_r : nullptr;
+      o.carried_r = static_cast<const uint32_t*>(tr.cols[0]);
+      o.carried_s = static_cast<const uint32_t*>(ts.cols[0]);
+    } else {
+      o.nr = (int)R->npay;
+      o.ns = (int)S->npay;
+      for (uint32_t c = 0; c < R->npay; ++c) {
+        o.r_src[c] = tr.cols[c];
+        o.r_dst[c] = res->pay[c];
+        o.r_bytes[c] = R->pay_bytes[c];
+      }
+      for (uint32_t c = 0; c < S->npay; ++c) {
+        o.s_src[c] = ts.cols[c];
+        o.s_dst[c] = res->pay[R->npay + c];
+        o.s_bytes[c] = S->pay_bytes[c];
+      }
+    }
+    if (opt->algo == CJ_SMJ)
+      return smj_find(ctx, tr.keys, R->rows, ts.keys, S->rows, kb, pk_fk, o, capacity);
+    return phj_find(ctx, tr.keys, tr.offsets, ts.keys, ts.offsets, fanout, kb,
+                    opt->sub_partition_limit, o, capacity);
+  };
+  alloc_output(ctx, R, S, cap, want_ids || gfur, res);
+  uint64_t total;
+  try {
+    total = find(cap);
+  } catch (const Error& e) {
+    if (e.code != CJ_ERR_CAPACITY_EXCEEDED || !pk_fk) throw;
+    free_output(ctx, res);
+    cap = count();
+    alloc_output(ctx, R, S, cap, want_ids || gfur, res);
+    total = find(cap);
+  }
+  if (ctx->timing) {  // algorithmic bytes of the find launch, now that |T| is known
+    uint64_t rrow = kb, srow = kb, out_row = kb + (want_ids || gfur ? 8 : 0);
+    if (!gfur) {
+      for (uint32_t c = 0; c < R->npay; ++c) rrow += R->pay_bytes[c];
+      for (uint32_t c = 0; c < S->npay; ++c) srow += S->pay_bytes[c];
+      out_row += rrow + srow - 2 * kb;
+    }
+    const uint64_t b = rrow * R->rows + srow * S->rows + out_row * total + (gfur ? 8 * total : 0);
+    ctx->set_bytes(opt->algo == CJ_SMJ ? "smj_find" : "phj_find", b);
+  }
+  tm.mark(2);
+
+  // ---- materialise (GFUR: gathers from the untransformed relations) -------
+  if (gfur) {
+    const void* in[2 * CJ_MAX_COLS];
+    void* out[2 * CJ_MAX_COLS];
+    uint32_t by[2 * CJ_MAX_COLS];
+    for (uint32_t c = 0; c < R->npay; ++c) {
+      in[c] = R->pay[c];
+      out[c] = res->pay[c];
+      by[c] = R->pay_bytes[c];
+    }
+    gather_cols(ctx, in, R->rows, res->ids_r, total, out, by, (int)R->npay);
+    for (uint32_t c = 0; c < S->npay; ++c) {
+      in[c] = S->pay[c];
+      out[c] = res->pay[R->npay + c];
+      by[c] = S->pay_bytes[c];
+    }
+    gather_cols(ctx, in, S->rows, res->ids_s, total, out, by, (int)S->npay);
+  }
+  tm.mark(3);
+  CJ_CUDA(cudaStreamSynchronize(ctx->stream));
+  raise_device_errors(ctx);
+  res->rows = total;
+  res->transform_ns = tm.ns(0, 1);
+  res->find_ns = tm.ns(1, 2);
+  res->materialize_ns = tm.ns(2, 3);
+  if (opt->want_stats) {
+    res->clusteredness_r = clusteredness(ctx, res->ids_r, total);
+    res->clusteredness_s = clusteredness(ctx, res->ids_s, total);
+  }
+  if (!want_ids && res->ids_r) {
+    ctx->release(res->ids_r);
+    ctx->release(res->ids_s);
+    res->ids_r = res->ids_s = nullptr;
+  }
+}
+
+// Runs fn, mapping exceptions to status codes (the C boundary).
+template <class F>
+int guarded(cj_ctx* ctx, F&& fn) {
+  try {
+    fn();
+    return CJ_OK;
+  } catch (const Error& e) {
+    if (ctx) ctx->last_error = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    if (ctx) ctx->last_error = "host allocation failed";
+    return CJ_ERR_OUT_OF_MEMORY;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->last_error = e.what();
+    return CJ_ERR_CUDA;
+  }
+}
+
+}  // namespace
+}  // namespace cj
+
+// ---- cj_ctx -------------------------------------------------------------------
+
+void* cj_ctx::alloc(uint64_t bytes) {
+  void* p = nullptr;
+  cj::check_cuda(cudaMallocAsync(&p, bytes ? bytes : 16, stream), "cudaMallocAsync");
+  return p;
+}
+
+void cj_ctx::release(void* p) {
+  if (p) cudaFreeAsync(p, stream);
+}
+
+uint16_t cj_ctx::next_epoch() {
+  if (epoch == 0xffff) {  // wrap: clear old generations
+    epoch = 0;
+    if (status) cj::check_cuda(cudaMemsetAsync(status, 0, status_words * 8, stream), "memset");
+  }
+  return ++epoch;
+}
+
+uint64_t* cj_ctx::status_buffer(uint64_t words) {
+  if (words > status_words) {
+    if (status) cudaFreeAsync(status, stream);
+    const uint64_t w = std::max<uint64_t>(words + words / 4, 1 << 16);
+    status = static_cast<uint64_t*>(alloc(w * 8));
+    cj::check_cuda(cudaMemsetAsync(status, 0, w * 8, stream), "memset status");
+    status_words = w;
+  }
+  return status;
+}
+
+cudaEvent_t cj_ctx::take_event() {
+  if (ev_used == ev_pool.size()) {
+    cudaEvent_t e;
+    cj::check_cuda(cudaEventCreate(&e), "cudaEventCreate");
+    ev_pool.push_back(e);
+  }
+  return ev_pool[ev_used++];
+}
+
+void cj_ctx::kbegin(const char* name, uint64_t alg_bytes) {
+  ++launches;
+  if (!timing) return;
+  KernelRec r{name, take_event(), take_event(), alg_bytes};
+  cj::check_cuda(cudaEventRecord(r.a, stream), "cudaEventRecord");
+  recs.push_back(r);
+}
+
+void cj_ctx::kend() {
+  if (!timing || recs.empty()) return;
+  cj::check_cuda(cudaEventRecord(recs.back().b, stream), "cudaEventRecord");
+}
+
+void cj_ctx::set_bytes(const char* name, uint64_t bytes) {
+  for (size_t i = recs.size(); i-- > 0;)
+    if (std::strcmp(recs[i].name, name) == 0) {
+      recs[i].bytes = bytes;
+      return;
+    }
+}
+
+uint32_t* cj_ctx::ticket(int slot) {
+  cj::check_cuda(cudaMemsetAsync(counters + slot, 0, sizeof(uint32_t), stream), "memset ticket");
+  return counters + slot;
+}
+
+// ---- C ABI --------------------------------------------------------------------
+
+extern "C" {
+
+int cj_ctx_create(int device, void* stream, cj_ctx** out) {
+  if (!out) return CJ_ERR_SPEC_INVALID;
+  *out = nullptr;
+  cj_ctx* ctx = new cj_ctx();
+  const int st = cj::guarded(ctx, [&] {
+    int ndev = 0;
+    CJ_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) cj::fail(CJ_ERR_CUDA, "no such CUDA device");
+    CJ_CUDA(cudaSetDevice(device));
+    ctx->device = device;
+    CJ_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
+    if (stream) {
+      ctx->stream = static_cast<cudaStream_t>(stream);
+    } else {
+      CJ_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+      ctx->own_stream = true;
+    }
+    cudaMemPool_t pool;
+    CJ_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    CJ_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    ctx->counters = static_cast<uint32_t*>(ctx->alloc(256 * sizeof(uint32_t)));
+    CJ_CUDA(cudaMemsetAsync(ctx->counters, 0, 256 * sizeof(uint32_t), ctx->stream));
+    ctx->err_word = ctx->counters + 128;
+    CJ_CUDA(cudaMallocHost(&ctx->host_pinned, 1 << 16));
+    for (auto& e : ctx->marks) CJ_CUDA(cudaEventCreate(&e));
+    CJ_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+  if (st != CJ_OK) {
+    std::fprintf(stderr, "cj_ctx_create: %s\n", ctx->last_error.c_str());
+    delete ctx;
+    return st;
+  }
+  *out = ctx;
+  return CJ_OK;
+}
+
+int cj_ctx_destroy(cj_ctx* ctx) {
+  if (!ctx) return CJ_OK;
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->status) cudaFreeAsync(ctx->status, ctx->stream);
+  if (ctx->counters) cudaFreeAsync(ctx->counters, ctx->stream);
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->host_pinned) cudaFreeHost(ctx->host_pinned);
+  for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  for (auto& e : ctx->marks)
+    if (e) cudaEventDestroy(e);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return CJ_OK;
+}
+
+const char* cj_last_error(const cj_ctx* ctx) { return ctx ? ctx->last_error.c_str() : "no ctx"; }
+
+int cj_sync(cj_ctx* ctx) {
+  return cj::guarded(ctx, [&] { CJ_CUDA(cudaStreamSynchronize(ctx->stream)); });
+}
+
+int cj_free(cj_ctx* ctx, void* p) {
+  return cj::guarded(ctx, [&] { ctx->release(p); });
+}
+
+int cj_alloc(cj_ctx* ctx, uint64_t bytes, void** p) {
+  return cj::guarded(ctx, [&] { *p = ctx->alloc(bytes); });
+}
+
+uint64_t cj_launch_count(const cj_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int cj_mark(cj_ctx* ctx, int slot) {
+  return cj::guarded(ctx, [&] {
+    if (slot < 0 || slot >= 16) cj::fail(CJ_ERR_SPEC_INVALID, "mark slot out of range");
+    CJ_CUDA(cudaEventRecord(ctx->marks[slot], ctx->stream));
+  });
+}
+
+int cj_elapsed_ms(cj_ctx* ctx, int a, int b, float* ms) {
+  return cj::guarded(ctx, [&] {
+    if (a < 0 || a >= 16 || b < 0 || b >= 16) cj::fail(CJ_ERR_SPEC_INVALID, "mark slot");
+    CJ_CUDA(cudaEventElapsedTime(ms, ctx->marks[a], ctx->marks[b]));
+  });
+}
+
+int cj_set_kernel_timing(cj_ctx* ctx, int on) {
+  return cj::guarded(ctx, [&] {
+    CJ_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->timing = on != 0;
+    ctx->recs.clear();
+    ctx->ev_used = 0;
+  });
+}
+
+int cj_kernel_records(cj_ctx* ctx, int max, const char** names, float* ms, uint64_t* bytes,
+                      int* count) {
+  return cj::guarded(ctx, [&] {
+    CJ_CUDA(cudaStreamSynchronize(ctx->stream));
+    const int n = (int)std::min<size_t>(ctx->recs.size(), (size_t)std::max(max, 0));
+    for (int i = 0; i < n; ++i) {
+      const auto& r = ctx->recs[i];
+      names[i] = r.name;
+      CJ_CUDA(cudaEventElapsedTime(&ms[i], r.a, r.b));
+      bytes[i] = r.bytes;
+    }
+    *count = (int)ctx->recs.size();
+  });
+}
+
+int cj_histogram(cj_ctx* ctx, const void* keys, uint64_t n, uint32_t kb, uint32_t lo,
+                 uint32_t hi, uint32_t* counts_host) {
+  return cj::guarded(ctx, [&] {
+    cj::check_key_bytes(kb);
+    if (hi < lo || hi - lo > 8) cj::fail(CJ_ERR_FANOUT_TOO_LARGE, "radix pass limited to 8 bits (256 partitions)");
+    if (hi > kb * 8) cj::fail(CJ_ERR_FANOUT_TOO_LARGE, "bit range exceeds key width");
+    cj::PassPlan plan;
+    plan.npasses = 1;
+    plan.lo[0] = lo;
+    plan.hi[0] = hi;
+    cj::Scratch cnt(ctx, 4 * cj::kRadix), base(ctx, 8 * cj::kRadix);
+    std::vector<uint32_t> h;
+    cj::histogram_passes(ctx, keys, n, (int)kb, plan, cnt.as<uint32_t>(), base.as<uint64_t>(), &h);
+    std::memcpy(counts_host, h.data(), sizeof(uint32_t) * (1u << (hi - lo)));
+  });
+}
+
+static cj::ValCols make_vals(const void* const* in, void* const* out, const uint32_t* bytes,
+                             uint32_t n, int gen_ids) {
+  if (n > CJ_MAX_COLS + 1) cj::fail(CJ_ERR_UNSUPPORTED, "too many value columns");
+  cj::ValCols v;
+  v.n = (int)n;
+  v.gen_ids = gen_ids;
+  for (uint32_t c = 0; c < n; ++c) {
+    v.in[c] = in ? in[c] : nullptr;
+    v.out[c] = out[c];
+    v.bytes[c] = bytes[c];
+    if (bytes[c] != 4 && bytes[c] != 8) cj::fail(CJ_ERR_KIND, "value columns must be 4 or 8 bytes");
+  }
+  if (gen_ids && (n == 0 || bytes[0] != 4)) cj::fail(CJ_ERR_KIND, "generated ids are u32");
+  return v;
+}
+
+int cj_radix_partition(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, uint32_t kb,
+                       uint32_t lo, uint32_t hi, const void* const* vin, void* const* vout,
+                       const uint32_t* vbytes, uint32_t nvals, uint64_t* offsets_host) {
+  return cj::guarded(ctx, [&] {
+    cj::check_key_bytes(kb);
+    if (hi < lo || hi - lo > 8) cj::fail(CJ_ERR_FANOUT_TOO_LARGE, "radix pass limited to 8 bits (256 partitions)");
+    if (hi > kb * 8) cj::fail(CJ_ERR_FANOUT_TOO_LARGE, "bit range exceeds key width");
+    cj::ValCols v = make_vals(vin, vout, vbytes, nvals, 0);
+    if (lo == hi) {  // fan-out 1 = identity (primitives.cpp:300-305)
+      cj::copy_columns(ctx, keys, keys_out, n, (int)kb, v);
+      if (offsets_host) {
+        offsets_host[0] = 0;
+        offsets_host[1] = n;
+      }
+      CJ_CUDA(cudaStreamSynchronize(ctx->stream));
+      return;
+    }
+    cj::PassPlan plan;
+    plan.npasses = 1;
+    plan.lo[0] = lo;
+    plan.hi[0] = hi;
+    cj::Scratch cnt(ctx, 4 * cj::kRadix), base(ctx, 8 * cj::kRadix);
+    std::vector<uint32_t> h;
+    cj::histogram_passes(ctx, keys, n, (int)kb, plan, cnt.as<uint32_t>(), base.as<uint64_t>(), &h);
+    cj::scatter_pass(ctx, keys, keys_out, n, (int)kb, lo, hi, base.as<uint64_t>(), v);
+    if (offsets_host) {
+      const uint32_t fan = 1u << (hi - lo);
+      offsets_host[0] = 0;
+      for (uint32_t d = 0; d < fan; ++d) offsets_host[d + 1] = offsets_host[d] + h[d];
+    }
+    CJ_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int cj_radix_partition_passes(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n,
+                              uint32_t kb, const uint32_t* plan_lo, const uint32_t* plan_hi,
+                              uint32_t npasses, const void* const* vin, void* const* vout,
+                              const uint32_t* vbytes, uint32_t nvals, int gen_ids) {
+  return cj::guarded(ctx, [&] {
+    cj::check_key_bytes(kb);
+    if (npasses > CJ_MAX_PASSES) cj::fail(CJ_ERR_UNSUPPORTED, "plan longer than 8 passes");
+    cj::PassPlan plan;
+    plan.npasses = (int)npasses;
+    for (uint32_t p = 0; p < npasses; ++p) {
+      if (plan_hi[p] < plan_lo[p] || plan_hi[p] - plan_lo[p] > 8)
+        cj::fail(CJ_ERR_FANOUT_TOO_LARGE, "radix pass limited to 8 bits (256 partitions)");
+      if (plan_hi[p] > kb * 8) cj::fail(CJ_ERR_FANOUT_TOO_LARGE, "bit range exceeds key width");
+      plan.lo[p] = plan_lo[p];
+      plan.hi[p] = plan_hi[p];
+    }
+    cj::ValCols v = make_vals(vin, vout, vbytes, nvals, gen_ids);
+    cj::lsd_partition(ctx, keys, keys_out, n, (int)kb, plan, v);
+    CJ_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int cj_sort_pairs(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, uint32_t kb,
+                  const void* const* vin, void* const* vout, const uint32_t* vbytes,
+                  uint32_t nvals, int gen_ids) {
+  return cj::guarded(ctx, [&] {
+    cj::check_key_bytes(kb);
+    cj::ValCols v = make_vals(vin, vout, vbytes, nvals, gen_ids);
+    cj::lsd_partition(ctx, keys, keys_out, n, (int)kb, cj::full_width_plan((int)kb), v);
+    CJ_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int cj_gather(cj_ctx* ctx, const void* const* in, uint64_t n_in, const uint32_t* map,
+              uint64_t m, void* const* out, const uint32_t* bytes, uint32_t ncols) {
+  return cj::guarded(ctx, [&] {
+    for (uint32_t c = 0; c < ncols; ++c)
+      if (bytes[c] != 4 && bytes[c] != 8) cj::fail(CJ_ERR_KIND, "gather columns must be 4 or 8 bytes");
+    cj::gather_cols(ctx, in, n_in, map, m, out, bytes, (int)ncols);
+    cj::raise_device_errors(ctx);
+  });
+}
+
+int cj_partition_relation(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, uint32_t kb,
+                          uint32_t total_bits, uint32_t bits_per_pass, const void* const* vin,
+                          void* const* vout, const uint32_t* vbytes, uint32_t nvals, int gen_ids,
+                          uint64_t* offsets_dev) {
+  return cj::guarded(ctx, [&] {
+    cj::check_key_bytes(kb);
+    if (total_bits > 20) cj::fail(CJ_ERR_FANOUT_TOO_LARGE, "partition fan-out capped at 2^20");
+    if (total_bits > kb * 8) cj::fail(CJ_ERR_FANOUT_TOO_LARGE, "partition bits exceed key width");
+    cj::ValCols v = make_vals(vin, vout, vbytes, nvals, gen_ids);
+    if (total_bits == 0) {
+      cj::copy_columns(ctx, keys, keys_out, n, (int)kb, v);
+    } else {
+      cj::lsd_any(ctx, keys, keys_out, n, (int)kb, cj::plan_bits(total_bits, bits_per_pass), v);
+    }
+    cj::partition_offsets(ctx, keys_out, n, (int)kb, total_bits, offsets_dev);
+    CJ_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int cj_hash_find_matches(cj_ctx* ctx, const cj_partitioned* b, const cj_partitioned* p,
+                         uint32_t fanout, uint32_t kb, uint32_t limit, int id_mode,
+                         uint64_t* total_host, void** keys_out, uint32_t** ids_r_out,
+                         uint32_t** ids_s_out) {
+  return cj::guarded(ctx, [&] {
+    cj::check_key_bytes(kb);
+    const bool phys = id_mode == CJ_IDS_PHYSICAL;
+    if (phys && (!b->carried || !p->carried))
+      cj::fail(CJ_ERR_UNSUPPORTED, "physical id mode needs carried id columns on both sides");
+    const uint64_t total = cj::phj_count(ctx, b->keys, b->offsets, p->keys, p->offsets, fanout,
+                                         (int)kb, limit);
+    void* k = ctx->alloc(std::max<uint64_t>(total, 1) * kb);
+    uint32_t* ir = static_cast<uint32_t*>(ctx->alloc(std::max<uint64_t>(total, 1) * 4));
+    uint32_t* is = static_cast<uint32_t*>(ctx->alloc(std::max<uint64_t>(total, 1) * 4));
+    cj::OutSpec o;
+    o.key = k;
+    o.ids_r = ir;
+    o.ids_s = is;
+    if (phys) {
+      o.carried_r = b->carried;
+      o.carried_s = p->carried;
+    }
+    cj::phj_find(ctx, b->keys, b->offsets, p->keys, p->offsets, fanout, (int)kb, limit, o, total);
+    *total_host = total;
+    *keys_out = k;
+    *ids_r_out = ir;
+    *ids_s_out = is;
+  });
+}
+
+int cj_merge_find_matches(cj_ctx* ctx, const void* r, uint64_t nr, const void* s, uint64_t ns,
+                          uint32_t kb, int pk_fk, int validate, uint64_t* total_host,
+                          void** keys_out, uint32_t** ids_r_out, uint32_t** ids_s_out) {
+  return cj::guarded(ctx, [&] {
+    cj::check_key_bytes(kb);
+    if (validate) {
+      cj::check_sorted(ctx, r, nr, (int)kb, false, CJ_ERR_NOT_SORTED, "build");
+      cj::check_sorted(ctx, s, ns, (int)kb, false, CJ_ERR_NOT_SORTED, "probe");
+      if (pk_fk) cj::check_sorted(ctx, r, nr, (int)kb, true, CJ_ERR_DUPLICATE_BUILD_KEYS, "pk");
+    }
+    const uint64_t total = cj::smj_count(ctx, r, nr, s, ns, (int)kb, pk_fk != 0);
+    void* k = ctx->alloc(std::max<uint64_t>(total, 1) * kb);
+    uint32_t* ir = static_cast<uint32_t*>(ctx->alloc(std::max<uint64_t>(total, 1) * 4));
+    uint32_t* is = static_cast<uint32_t*>(ctx->alloc(std::max<uint64_t>(total, 1) * 4));
+    cj::OutSpec o;
+    o.key = k;
+    o.ids_r = ir;
+    o.ids_s = is;
+    cj::smj_find(ctx, r, nr, s, ns, (int)kb, pk_fk != 0, o, total);
+    *total_host = total;
+    *keys_out = k;
+    *ids_r_out = ir;
+    *ids_s_out = is;
+  });
+}
+
+void cj_default_options(cj_join_options* o) {
+  std::memset(o, 0, sizeof(*o));
+  o->algo = CJ_PHJ;
+  o->pattern = CJ_GFTR;
+  o->radix_bits_per_pass = 8;
+  o->total_radix_bits = -1;
+  o->sub_partition_limit = 4096;
+}
+
+int cj_run_join(cj_ctx* ctx, const cj_relation* build, const cj_relation* probe,
+                const cj_join_options* opt, cj_join_result* res) {
+  return cj::guarded(ctx, [&] {
+    try {
+      cj::run_join_dev(ctx, build, probe, opt, res);
+    } catch (...) {
+      cj::free_output(ctx, res);
+      throw;
+    }
+  });
+}
+
+int cj_result_free(cj_ctx* ctx, cj_join_result* res) {
+  return cj::guarded(ctx, [&] { cj::free_output(ctx, res); });
+}
+
+int cj_run_join_host(cj_ctx* ctx, const cj_relation* build, const cj_relation* probe,
+                     const cj_join_options* opt, cj_host_alloc_fn alloc, void* user,
+                     cj_join_result* out, uint64_t* h2d_ns, uint64_t* d2h_ns) {
+  return cj::guarded(ctx, [&] {
+    cj::validate_relation(build, "a build relation");
+    cj::validate_relation(probe, "a probe relation");
+    std::vector<void*> owned;
+    struct G {
+      cj_ctx* c;
+      std::vector<void*>* v;
+      ~G() {
+        for (void* p : *v) c->release(p);
+      }
+    } g{ctx, &owned};
+    cj::Timer tm(ctx);
+    auto up = [&](const cj_relation* h, cj_relation* d) {
+      *d = *h;
+      void* k = ctx->alloc(std::max<uint64_t>(h->rows * h->key_bytes, 16));
+      owned.push_back(k);
+      if (h->rows)
+        CJ_CUDA(cudaMemcpyAsync(k, h->key, h->rows * h->key_bytes, cudaMemcpyHostToDevice,
+                                ctx->stream));
+      d->key = k;
+      for (uint32_t c = 0; c < h->npay; ++c) {
+        void* p = ctx->alloc(std::max<uint64_t>(h->rows * h->pay_bytes[c], 16));
+        owned.push_back(p);
+        if (h->rows)
+          CJ_CUDA(cudaMemcpyAsync(p, h->pay[c], h->rows * h->pay_bytes[c],
+                                  cudaMemcpyHostToDevice, ctx->stream));
+        d->pay[c] = p;
+      }
+    };
+    cj_relation R, S;
+    tm.mark(0);
+    up(build, &R);
+    up(probe, &S);
+    tm.mark(1);
+    cj_join_result dres;
+    std::memset(&dres, 0, sizeof(dres));
+    cj::run_join_dev(ctx, &R, &S, opt, &dres);
+    struct RG {
+      cj_ctx* c;
+      cj_join_result* r;
+      ~RG() { cj::free_output(c, r); }
+    } rg{ctx, &dres};
+    *out = dres;
+    const uint64_t t = dres.rows;
+    tm.mark(2);
+    auto down = [&](const void* src, uint64_t bytes) -> void* {
+      void* h = alloc(std::max<uint64_t>(bytes, 1), user);
+      if (!h) cj::fail(CJ_ERR_OUT_OF_MEMORY, "host output allocation failed");
+      if (bytes) CJ_CUDA(cudaMemcpyAsync(h, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+      return h;
+    };
+    out->key = down(dres.key, t * build->key_bytes);
+    for (uint32_t c = 0; c < build->npay; ++c)
+      out->pay[c] = down(dres.pay[c], t * build->pay_bytes[c]);
+    for (uint32_t c = 0; c < probe->npay; ++c)
+      out->pay[build->npay + c] = down(dres.pay[build->npay + c], t * probe->pay_bytes[c]);
+    out->ids_r = dres.ids_r ? static_cast<uint32_t*>(down(dres.ids_r, t * 4)) : nullptr;
+    out->ids_s = dres.ids_s ? static_cast<uint32_t*>(down(dres.ids_s, t * 4)) : nullptr;
+    tm.mark(3);
+    CJ_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (h2d_ns) *h2d_ns = tm.ns(0, 1);
+    if (d2h_ns) *d2h_ns = tm.ns(2, 3);
+  });
+}
+
+int cj_gen_pk_fk(cj_ctx* ctx, uint64_t r_rows, uint64_t s_rows, uint32_t r_pay, uint32_t s_pay,
+                 uint32_t key_bytes, uint32_t pay_bytes, double match_ratio, double zipf,
+                 uint64_t seed, void* r_key, void* const* r_pays, void* s_key,
+                 void* const* s_pays) {
+  return cj::guarded(ctx, [&] {
+    cj::gen_pk_fk(ctx, r_rows, s_rows, r_pay, s_pay, key_bytes, pay_bytes, match_ratio, zipf,
+                  seed, r_key, r_pays, s_key, s_pays);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,183 @@
+// Workload generation bit-identical to the reference's workloads::gen_pk_fk
+// (workloads.cpp:89-133) and its counter RNG (rng.hpp:8-37).
+//
+// The Fisher-Yates permutation (workloads.cpp:26-34) and the Zipf CDF
+// (workloads.cpp:60-70, a sequential double accumulation) are sequential by
+// definition and run on the host; every per-draw quantity (uniform / Zipf
+// foreign keys, key displacement, payload streams) is a pure function of
+// (stream, index) and is generated on the device.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <vector>
+
+#include "cj_internal.cuh"
+
+namespace cj {
+namespace {
+
+constexpr uint64_t kGold = 0x9E3779B97F4A7C15ull;
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t stream_of(uint64_t seed, uint64_t tag) {
+  return mix64(seed ^ mix64(tag + kGold));
+}
+__host__ __device__ __forceinline__ uint64_t rng_at(uint64_t seed, uint64_t i) {
+  return mix64(seed + (i + 1) * kGold);
+}
+__host__ __device__ __forceinline__ double rng_u01(uint64_t seed, uint64_t i) {
+  return static_cast<double>(rng_at(seed, i) >> 11) * 0x1.0p-53;
+}
+__host__ __forceinline__ uint64_t rng_below(uint64_t seed, uint64_t i, uint64_t bound) {
+  return static_cast<uint64_t>((static_cast<unsigned __int128>(rng_at(seed, i)) * bound) >> 64);
+}
+
+std::vector<uint32_t> permutation(uint64_t n, uint64_t seed) {
+  std::vector<uint32_t> p(n);
+  for (uint64_t i = 0; i < n; ++i) p[i] = static_cast<uint32_t>(i);
+  for (uint64_t i = n; i > 1; --i) {
+    const uint64_t j = rng_below(seed, i, i);
+    std::swap(p[i - 1], p[j]);
+  }
+  return p;
+}
+
+template <class K>
+__global__ void k_rkeys(const uint32_t* __restrict__ perm, uint64_t n, uint64_t keep, K* out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t v = perm[i];
+    if (v >= keep) v += n;  // workloads.cpp:113-120
+    out[i] = (K)v;
+  }
+}
+
+template <class K>
+__global__ void k_skeys_uniform(uint64_t seed, uint64_t n_r, uint64_t n_s, K* out) {
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_s;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    const double u = rng_u01(seed, j);
+    uint64_t r = static_cast<uint64_t>(__dmul_rn(u, static_cast<double>(n_r)));
+    if (r >= n_r) r = n_r - 1;
+    out[j] = (K)r;
+  }
+}
+
+template <class K>
+__global__ void k_skeys_zipf(uint64_t seed, const double* __restrict__ cdf,
+                             const uint32_t* __restrict__ rank_to_key, uint64_t n_r, uint64_t n_s,
+                             K* out) {
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_s;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    const double u = rng_u01(seed, j);
+    uint64_t lo = 0, hi = n_r;  // upper_bound: first cdf > u
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (cdf[mid] > u) hi = mid; else lo = mid + 1;
+    }
+    const uint64_t rank = lo == n_r ? n_r - 1 : lo;
+    out[j] = (K)rank_to_key[rank];
+  }
+}
+
+template <class T>
+__global__ void k_payload(uint64_t seed, uint64_t n, T* out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = (T)rng_at(seed, i);
+}
+
+}  // namespace
+
+void gen_pk_fk(cj_ctx* ctx, uint64_t r_rows, uint64_t s_rows, uint32_t r_pay, uint32_t s_pay,
+               uint32_t key_bytes, uint32_t pay_bytes, double match_ratio, double zipf,
+               uint64_t seed, void* r_key, void* const* r_pays, void* s_key,
+               void* const* s_pays) {
+  if (match_ratio < 0.0 || match_ratio > 1.0) fail(CJ_ERR_SPEC_INVALID, "match ratio must lie in [0, 1]");
+  if (zipf < 0.0) fail(CJ_ERR_SPEC_INVALID, "zipf factor must be >= 0");
+  if (r_rows > 0x7fffffffull || s_rows > 0x7fffffffull)
+    fail(CJ_ERR_SPEC_INVALID, "row count exceeds the 2^31-1 cap");
+  if ((key_bytes != 4 && key_bytes != 8) || (pay_bytes != 4 && pay_bytes != 8))
+    fail(CJ_ERR_KIND, "key/payload widths must be 4 or 8 bytes");
+  const unsigned grid = ctx->num_sms * 8;
+  // R keys: shuffled dense domain [0, |R|), non-kept keys displaced by |R|
+  const std::vector<uint32_t> perm = permutation(r_rows, stream_of(seed, 0x52000001ull));
+  const uint64_t keep = static_cast<uint64_t>(std::llround(match_ratio * static_cast<double>(r_rows)));
+  {
+    Scratch dperm(ctx, r_rows * 4);
+    if (r_rows) {
+      CJ_CUDA(cudaMemcpyAsync(dperm.p, perm.data(), r_rows * 4, cudaMemcpyHostToDevice, ctx->stream));
+      ctx->kbegin("gen_rkeys", r_rows * (4 + key_bytes));
+      if (key_bytes == 4)
+        k_rkeys<uint32_t><<<grid, 256, 0, ctx->stream>>>(dperm.as<uint32_t>(), r_rows, keep,
+                                                         static_cast<uint32_t*>(r_key));
+      else
+        k_rkeys<uint64_t><<<grid, 256, 0, ctx->stream>>>(dperm.as<uint32_t>(), r_rows, keep,
+                                                         static_cast<uint64_t*>(r_key));
+      ctx->kend();
+    }
+    CJ_CUDA(cudaStreamSynchronize(ctx->stream));  // perm host buffer lifetime
+  }
+  // S keys (workloads.cpp:55-81, 98-111)
+  const uint64_t zseed = stream_of(seed, 0x5a1bf001ull);
+  if (r_rows > 0 && s_rows > 0) {
+    if (zipf == 0.0) {
+      ctx->kbegin("gen_skeys", s_rows * key_bytes);
+      if (key_bytes == 4)
+        k_skeys_uniform<uint32_t><<<grid, 256, 0, ctx->stream>>>(zseed, r_rows, s_rows,
+                                                                 static_cast<uint32_t*>(s_key));
+      else
+        k_skeys_uniform<uint64_t><<<grid, 256, 0, ctx->stream>>>(zseed, r_rows, s_rows,
+                                                                 static_cast<uint64_t*>(s_key));
+      ctx->kend();
+    } else {
+      std::vector<double> cdf(r_rows);
+      double acc = 0.0;
+      for (uint64_t k = 0; k < r_rows; ++k) {
+        acc += std::pow(static_cast<double>(k + 1), -zipf);
+        cdf[k] = acc;
+      }
+      const double norm = 1.0 / acc;
+      for (auto& v : cdf) v *= norm;
+      cdf.back() = 1.0;
+      const std::vector<uint32_t> r2k = permutation(r_rows, stream_of(seed, 0x53000001ull));
+      Scratch dcdf(ctx, r_rows * 8), dr2k(ctx, r_rows * 4);
+      CJ_CUDA(cudaMemcpyAsync(dcdf.p, cdf.data(), r_rows * 8, cudaMemcpyHostToDevice, ctx->stream));
+      CJ_CUDA(cudaMemcpyAsync(dr2k.p, r2k.data(), r_rows * 4, cudaMemcpyHostToDevice, ctx->stream));
+      ctx->kbegin("gen_skeys_zipf", s_rows * key_bytes);
+      if (key_bytes == 4)
+        k_skeys_zipf<uint32_t><<<grid, 256, 0, ctx->stream>>>(zseed, dcdf.as<double>(),
+                                                              dr2k.as<uint32_t>(), r_rows, s_rows,
+                                                              static_cast<uint32_t*>(s_key));
+      else
+        k_skeys_zipf<uint64_t><<<grid, 256, 0, ctx->stream>>>(zseed, dcdf.as<double>(),
+                                                              dr2k.as<uint32_t>(), r_rows, s_rows,
+                                                              static_cast<uint64_t*>(s_key));
+      ctx->kend();
+      CJ_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+  } else if (s_rows > 0) {
+    CJ_CUDA(cudaMemsetAsync(s_key, 0, s_rows * key_bytes, ctx->stream));
+  }
+  // payload streams 0x7000+c (R) / 0x8000+c (S), truncated to the width
+  auto pay = [&](void* dst, uint64_t n, uint64_t tag) {
+    if (n == 0) return;
+    const uint64_t sd = stream_of(seed, tag);
+    ctx->kbegin("gen_payload", n * pay_bytes);
+    if (pay_bytes == 4)
+      k_payload<uint32_t><<<grid, 256, 0, ctx->stream>>>(sd, n, static_cast<uint32_t*>(dst));
+    else
+      k_payload<uint64_t><<<grid, 256, 0, ctx->stream>>>(sd, n, static_cast<uint64_t*>(dst));
+    ctx->kend();
+  };
+  for (uint32_t c = 0; c < r_pay; ++c) pay(r_pays[c], r_rows, 0x7000ull + c);
+  for (uint32_t c = 0; c < s_pay; ++c) pay(s_pays[c], s_rows, 0x8000ull + c);
+  CJ_CUDA(cudaGetLastError());
+  CJ_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+}  // namespace cj

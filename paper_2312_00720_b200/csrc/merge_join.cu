@@ -1,0 +1,318 @@
+// Sort-merge join find phase (K5), optionally fused with GFTR
+// materialisation.
+//
+// Reference semantics (paths relative to the reference's proj/):
+//   merge_path_split / diagonal_intersect  merge_match.cpp:30-48, 75-102
+//   walk_part                              merge_match.cpp:53-71
+//   merge_match_count / merge_match_fill   merge_match.cpp:104-155
+// Output: every (i, j) with r[i] == s[j] in (s-position, r-position) order,
+// output key = s[j]; pk_fk emits only the lower bound (merge_match.cpp:65-68).
+//
+// Design (B200): persistent CTAs take tiles of 2048 consecutive probe (s)
+// positions in ticket order.  A tile's r window [lower_bound(s[j0]),
+// upper_bound(s[j1-1])) is found by two global binary searches and staged in
+// shared memory (merge path: equal work per tile on the s side, the window
+// bounded by the keys the tile can match); every probe then finds its r run by
+// a shared-memory binary search.  Per-tile match counts are chained by
+// warp-cooperative decoupled look-back, so rows land at their reference
+// positions in one pass.  Windows larger than shared memory fall back to
+// global binary search (correct, slower; only for sparse probes).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "cj_device.cuh"
+#include "cj_internal.cuh"
+
+namespace cj {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr uint32_t kTileS = 2048;
+
+struct SmjArgs {
+  const void* r;
+  uint64_t nr;
+  const void* s;
+  uint64_t ns;
+  int pk_fk;
+  uint32_t wmax;          // shared-memory r window capacity (keys)
+  uint64_t tiles;
+  uint64_t* status;
+  uint64_t epoch;
+  uint32_t* ticket;
+  uint32_t* err;
+  uint64_t capacity;
+  int write;
+  uint64_t* total_out;
+  void* key_out;
+  uint32_t* ids_r;
+  uint32_t* ids_s;
+  const uint32_t* carried_r;
+  const uint32_t* carried_s;
+  int nr_cols, ns_cols;
+  const void* r_src[CJ_MAX_COLS];
+  const void* s_src[CJ_MAX_COLS];
+  void* r_dst[CJ_MAX_COLS];
+  void* s_dst[CJ_MAX_COLS];
+  uint32_t r_bytes[CJ_MAX_COLS];
+  uint32_t s_bytes[CJ_MAX_COLS];
+};
+
+template <class K>
+__device__ __forceinline__ uint64_t g_lower_bound(const K* __restrict__ r, uint64_t lo,
+                                                  uint64_t hi, K k) {
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (r[mid] < k) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+template <class K>
+__device__ __forceinline__ uint64_t g_upper_bound(const K* __restrict__ r, uint64_t lo,
+                                                  uint64_t hi, K k) {
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (r[mid] <= k) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+template <class K>
+__device__ __forceinline__ void emit(const SmjArgs& a, uint64_t o, uint64_t i, uint64_t j, K k) {
+  if (a.key_out) static_cast<K*>(a.key_out)[o] = k;
+  if (a.ids_r) a.ids_r[o] = a.carried_r ? a.carried_r[i] : (uint32_t)i;
+  if (a.ids_s) a.ids_s[o] = a.carried_s ? a.carried_s[j] : (uint32_t)j;
+  for (int c = 0; c < a.nr_cols; ++c) {
+    if (a.r_bytes[c] == 4)
+      static_cast<uint32_t*>(a.r_dst[c])[o] = static_cast<const uint32_t*>(a.r_src[c])[i];
+    else
+      static_cast<uint64_t*>(a.r_dst[c])[o] = static_cast<const uint64_t*>(a.r_src[c])[i];
+  }
+  for (int c = 0; c < a.ns_cols; ++c) {
+    if (a.s_bytes[c] == 4)
+      static_cast<uint32_t*>(a.s_dst[c])[o] = __ldcs(static_cast<const uint32_t*>(a.s_src[c]) + j);
+    else
+      static_cast<uint64_t*>(a.s_dst[c])[o] = __ldcs(static_cast<const uint64_t*>(a.s_src[c]) + j);
+  }
+}
+
+template <class K>
+__global__ void __launch_bounds__(kThreads) k_smj_find(const __grid_constant__ SmjArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  K* rk = reinterpret_cast<K*>(smem);                          // [wmax]
+  uint32_t* loff = reinterpret_cast<uint32_t*>(smem + (size_t)a.wmax * sizeof(K));  // [kTileS]
+  uint32_t* mcnt = loff + kTileS;                              // [kTileS]
+  __shared__ uint64_t s_tile, s_lb0, s_w, s_base;
+  __shared__ uint64_t s_wcount[kWarps], s_wbase[kWarps];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const K* __restrict__ r = static_cast<const K*>(a.r);
+  const K* __restrict__ s = static_cast<const K*>(a.s);
+  while (true) {
+    if (tid == 0) {
+      const uint64_t t = atomicAdd(a.ticket, 1u);
+      s_tile = t;
+      if (t < a.tiles) {
+        const uint64_t j0 = t * kTileS, j1 = dev::umin64(a.ns, j0 + kTileS);
+        const uint64_t lb0 = g_lower_bound<K>(r, 0, a.nr, s[j0]);
+        const uint64_t ub1 = g_upper_bound<K>(r, lb0, a.nr, s[j1 - 1]);
+        s_lb0 = lb0;
+        s_w = ub1 - lb0;
+      }
+    }
+    __syncthreads();
+    const uint64_t t = s_tile;
+    if (t >= a.tiles) break;
+    const uint64_t j0 = t * kTileS;
+    const uint32_t nq = (uint32_t)dev::umin64(kTileS, a.ns - j0);
+    const uint64_t lb0 = s_lb0, w = s_w;
+    const bool windowed = w <= a.wmax;
+    if (windowed)
+      for (uint32_t i = tid; i < w; i += kThreads) rk[i] = r[lb0 + i];
+    __syncthreads();
+
+    const uint32_t rounds = (nq + 31) / 32;
+    const uint32_t r0 = rounds * warp / kWarps, r1 = rounds * (warp + 1) / kWarps;
+    uint64_t wc = 0;
+    for (uint32_t rr = r0; rr < r1; ++rr) {
+      const uint32_t jl = rr * 32 + lane;
+      if (jl < nq) {
+        const K k = s[j0 + jl];
+        uint64_t lb, m = 0;
+        if (windowed) {
+          uint32_t lo = 0, hi = (uint32_t)w;
+          while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (rk[mid] < k) lo = mid + 1; else hi = mid;
+          }
+          lb = lo;
+          if (lo < w && rk[lo] == k) {
+            if (a.pk_fk) {
+              m = 1;
+            } else {
+              uint32_t lo2 = lo + 1, hi2 = (uint32_t)w;
+              while (lo2 < hi2) {
+                const uint32_t mid = (lo2 + hi2) >> 1;
+                if (rk[mid] <= k) lo2 = mid + 1; else hi2 = mid;
+              }
+              m = lo2 - lo;
+            }
+          }
+        } else {
+          const uint64_t g = g_lower_bound<K>(r, lb0, lb0 + w, k);
+          lb = g - lb0;
+          if (g < a.nr && r[g] == k)
+            m = a.pk_fk ? 1 : g_upper_bound<K>(r, g, lb0 + w, k) - g;
+        }
+        loff[jl] = (uint32_t)lb;
+        mcnt[jl] = (uint32_t)m;
+        wc += m;
+      }
+    }
+    wc = dev::warp_sum(wc);
+    if (lane == 0) s_wcount[warp] = wc;
+    __syncthreads();
+    if (warp == 0) {
+      const uint64_t v = lane < kWarps ? s_wcount[lane] : 0;
+      const uint64_t inc = dev::warp_inclusive_sum(v);
+      if (lane < kWarps) s_wbase[lane] = inc - v;
+      const uint64_t tot = __shfl_sync(0xffffffffu, inc, kWarps - 1);
+      const uint64_t base = dev::warp_lookback(a.status, t, tot, a.epoch, a.err);
+      if (lane == 0) {
+        s_base = base;
+        if (t == a.tiles - 1) *a.total_out = base + tot;
+        if (a.write && base + tot > a.capacity) atomicOr(a.err, kErrOverflow);
+      }
+    }
+    __syncthreads();
+    if (a.write) {
+      uint64_t o = s_base + s_wbase[warp];
+      for (uint32_t rr = r0; rr < r1; ++rr) {
+        const uint32_t jl = rr * 32 + lane;
+        const uint32_t m = jl < nq ? mcnt[jl] : 0;
+        const uint32_t inc = dev::warp_inclusive_sum(m);
+        uint64_t oo = o + inc - m;
+        if (m) {
+          const uint64_t j = j0 + jl;
+          const K k = s[j];
+          const uint64_t i0 = lb0 + loff[jl];
+          for (uint32_t q = 0; q < m; ++q, ++oo)
+            if (oo < a.capacity) emit<K>(a, oo, i0 + q, j, k);
+        }
+        o += __shfl_sync(0xffffffffu, inc, 31);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <class K>
+__global__ void k_check_sorted(const K* __restrict__ v, uint64_t n, int strict,
+                               uint32_t* err, uint32_t code) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x + 1; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const K a = v[i - 1], b = v[i];
+    if (strict ? !(a < b) : (a > b)) {
+      atomicOr(err, code);
+      return;
+    }
+  }
+}
+
+template <class K>
+uint64_t run(cj_ctx* ctx, SmjArgs a) {
+  a.tiles = (a.ns + kTileS - 1) / kTileS;
+  Scratch tot(ctx, sizeof(uint64_t));
+  CJ_CUDA(cudaMemsetAsync(tot.p, 0, sizeof(uint64_t), ctx->stream));
+  a.total_out = tot.as<uint64_t>();
+  if (a.tiles > 0 && a.nr > 0) {
+    a.status = ctx->status_buffer(a.tiles);
+    a.epoch = ctx->next_epoch();
+    a.ticket = ctx->ticket(2);
+    a.err = ctx->err_word;
+    a.wmax = 8192;
+    const size_t smem = (size_t)a.wmax * sizeof(K) + 2 * sizeof(uint32_t) * kTileS;
+    CJ_CUDA(cudaFuncSetAttribute(k_smj_find<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    int per_sm = 0;
+    CJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_smj_find<K>, kThreads, smem));
+    per_sm = std::max(per_sm, 1);
+    const uint64_t grid = std::min<uint64_t>((uint64_t)ctx->num_sms * per_sm, a.tiles);
+    ctx->kbegin(a.write ? "smj_find" : "smj_count", 0);
+    k_smj_find<K><<<(unsigned)grid, kThreads, smem, ctx->stream>>>(a);
+    ctx->kend();
+    CJ_CUDA(cudaGetLastError());
+  }
+  uint64_t* h = reinterpret_cast<uint64_t*>(ctx->host_pinned);
+  CJ_CUDA(cudaMemcpyAsync(h, tot.p, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
+  CJ_CUDA(cudaStreamSynchronize(ctx->stream));
+  return h[0];
+}
+
+SmjArgs base(const void* rkeys, uint64_t nr, const void* skeys, uint64_t ns, bool pk_fk) {
+  SmjArgs a{};
+  a.r = rkeys;
+  a.nr = nr;
+  a.s = skeys;
+  a.ns = ns;
+  a.pk_fk = pk_fk ? 1 : 0;
+  return a;
+}
+
+}  // namespace
+
+uint64_t smj_find(cj_ctx* ctx, const void* rkeys, uint64_t nr, const void* skeys, uint64_t ns,
+                  int key_bytes, bool pk_fk, const OutSpec& out, uint64_t capacity) {
+  SmjArgs a = base(rkeys, nr, skeys, ns, pk_fk);
+  a.write = 1;
+  a.capacity = capacity;
+  a.key_out = out.key;
+  a.ids_r = out.ids_r;
+  a.ids_s = out.ids_s;
+  a.carried_r = out.carried_r;
+  a.carried_s = out.carried_s;
+  a.nr_cols = out.nr;
+  a.ns_cols = out.ns;
+  for (int c = 0; c < out.nr; ++c) {
+    a.r_src[c] = out.r_src[c];
+    a.r_dst[c] = out.r_dst[c];
+    a.r_bytes[c] = out.r_bytes[c];
+  }
+  for (int c = 0; c < out.ns; ++c) {
+    a.s_src[c] = out.s_src[c];
+    a.s_dst[c] = out.s_dst[c];
+    a.s_bytes[c] = out.s_bytes[c];
+  }
+  const uint64_t t = key_bytes == 4 ? run<uint32_t>(ctx, a) : run<uint64_t>(ctx, a);
+  raise_device_errors(ctx);
+  return t;
+}
+
+uint64_t smj_count(cj_ctx* ctx, const void* rkeys, uint64_t nr, const void* skeys, uint64_t ns,
+                   int key_bytes, bool pk_fk) {
+  SmjArgs a = base(rkeys, nr, skeys, ns, pk_fk);
+  a.write = 0;
+  return key_bytes == 4 ? run<uint32_t>(ctx, a) : run<uint64_t>(ctx, a);
+}
+
+void check_sorted(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes, bool strict,
+                  int err_code, const char* what) {
+  if (n < 2) return;
+  const uint32_t code = err_code == CJ_ERR_NOT_SORTED ? kErrNotSorted : kErrDupKeys;
+  const unsigned grid = grid_for(n, 256 * 8, ctx->num_sms * 8);
+  ctx->kbegin("check_sorted", n * key_bytes);
+  if (key_bytes == 4)
+    k_check_sorted<uint32_t><<<grid, 256, 0, ctx->stream>>>(static_cast<const uint32_t*>(keys), n,
+                                                           strict, ctx->err_word, code);
+  else
+    k_check_sorted<uint64_t><<<grid, 256, 0, ctx->stream>>>(static_cast<const uint64_t*>(keys), n,
+                                                           strict, ctx->err_word, code);
+  ctx->kend();
+  CJ_CUDA(cudaGetLastError());
+  (void)what;
+  raise_device_errors(ctx);
+}
+
+}  // namespace cj
