@@ -1,7 +1,7 @@
 /* cj_api.h — C-ABI of the B200-native equi-join path (libcoljoin_b200.so).
  *
  * This is the drop-in boundary: plain pointers and sizes, no C++ or torch
- * types.  The C++ host library (include/coljoin/*.hpp, libcoljoin_host) keeps
+ * types.  The C++ host library (include/coljoin/ headers, libcoljoin_host) keeps
  * the reference's operator API on top of it; other hosts bind these symbols
  * directly (ctypes / cgo / JNI — see INTEGRATION.md).
  *
@@ -68,6 +68,13 @@ int cj_sync(cj_ctx* ctx);
 int cj_free(cj_ctx* ctx, void* dev_ptr);
 /* Stream-ordered device allocation from the ctx pool (test/bench helper). */
 int cj_alloc(cj_ctx* ctx, uint64_t bytes, void** dev_ptr);
+/* Stream-ordered copy on the ctx stream; kind 1 = host->device, 2 =
+ * device->host, 3 = device->device.  Host->device/device->host copies are
+ * synchronous with respect to the host (the call returns when done). */
+int cj_copy(cj_ctx* ctx, void* dst, const void* src, uint64_t bytes, int kind);
+/* Peak device scratch (bytes) held by operators since the last reset; the
+ * host library charges it to the caller's Workspace ledger. */
+uint64_t cj_scratch_peak(cj_ctx* ctx, int reset);
 /* Kernel launches issued through this ctx since creation (bench evidence). */
 uint64_t cj_launch_count(const cj_ctx* ctx);
 /* Record (cudaEventRecord) a named timing mark on the ctx stream; elapsed ms
@@ -100,7 +107,7 @@ int cj_radix_partition(cj_ctx* ctx, const void* keys_dev, void* keys_out_dev, ui
                        const uint32_t* val_bytes, uint32_t nvals, uint64_t* offsets_host);
 
 /* radix_partition_passes(_keys) — primitives.hpp:52-59: stable LSD over the
- * plan, constant-digit passes skipped (primitives.cpp:217-256).
+ * plan (npasses <= 64), constant-digit passes skipped (primitives.cpp:217-256).
  * gen_ids != 0: value column 0 is not read but generated as the source row
  * index (u32) — GFUR's tuple ids born in pass 1 (join_engine.cpp:74-78). */
 int cj_radix_partition_passes(cj_ctx* ctx, const void* keys_dev, void* keys_out_dev, uint64_t n,
@@ -210,6 +217,28 @@ typedef void* (*cj_host_alloc_fn)(uint64_t bytes, void* user);
 int cj_run_join_host(cj_ctx* ctx, const cj_relation* build, const cj_relation* probe,
                      const cj_join_options* opt, cj_host_alloc_fn alloc, void* user,
                      cj_join_result* res_host, uint64_t* h2d_ns, uint64_t* d2h_ns);
+
+/* ---- multi-GPU radix sharding (no reference counterpart) ---- */
+/* Stable partition of a relation's rows by shard s(key) = floor(mix64(key) *
+ * parts / 2^64) (mix64 = rng.hpp:8-12), the send layout of the all-to-all
+ * shuffle: rows of shard d land contiguously, in input order, in shard order;
+ * counts_host[d] = rows of shard d.  Key-deterministic, so co-partitions of R
+ * and S meet on one GPU. */
+int cj_shard_partition(cj_ctx* ctx, const void* keys_dev, void* keys_out_dev, uint64_t n,
+                       uint32_t key_bytes, uint32_t parts, const void* const* vals_dev,
+                       void* const* vals_out_dev, const uint32_t* val_bytes, uint32_t nvals,
+                       uint64_t* counts_host);
+
+/* Weak-scaling shard generator: rank r of `ranks` gets |R|/ranks rows of a PK
+ * domain that is a bijective scramble of [0, |R|) (|R| a power of two; a
+ * 4-round Feistel permutation keyed by seed) and |S|/ranks uniform foreign
+ * keys over [0, |R|) from the counter RNG; payload c is the stream 0x7000+c /
+ * 0x8000+c at the global row index (workloads.cpp:124-129).  The reference
+ * generator is sequential and capped at 2^31-1 rows (workloads.cpp:26-51), so
+ * config C5 needs this one. */
+int cj_gen_shard(cj_ctx* ctx, uint64_t r_rows_total, uint64_t s_rows_total, uint32_t rank,
+                 uint32_t ranks, uint32_t r_pay, uint32_t s_pay, uint64_t seed, void* r_key_dev,
+                 void* const* r_pay_dev, void* s_key_dev, void* const* s_pay_dev);
 
 /* ---- workload generation (workloads.hpp:11-33 gen_pk_fk) ----------------- */
 /* Bit-identical to workloads::gen_pk_fk: the Fisher-Yates permutation and the

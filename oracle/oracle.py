@@ -28,6 +28,8 @@ def build() -> None:
     subprocess.run(["make", "-s", "-C", HERE, "port"], check=True)
     if os.path.isdir("/root/reference/proj/src"):
         subprocess.run(["make", "-s", "-j8", "-C", HERE, "ref"], check=True)
+        if os.path.exists(os.path.join(HERE, "..", "paper_2312_00720_b200", "libcoljoin_host.so")):
+            subprocess.run(["make", "-s", "-j8", "-C", HERE, "dropin"], check=True)
 
 
 def lib():

@@ -120,6 +120,15 @@ PROTOS = {
     "cj_run_join_host": (C.c_int, [_P, C.POINTER(Relation), C.POINTER(Relation),
                                    C.POINTER(JoinOptions), HOST_ALLOC, _P,
                                    C.POINTER(JoinResult), _U64P, _U64P]),
+    "cj_shard_partition": (C.c_int, [_P, _P, _P, C.c_uint64, C.c_uint32, C.c_uint32, _PP, _PP,
+                                     _U32P, C.c_uint32, _U64P]),
+    "cj_gen_shard": (C.c_int, [_P, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
+                               C.c_uint32, C.c_uint64, _P, _PP, _P, _PP]),
+    "cj_set_kernel_timing": (C.c_int, [_P, C.c_int]),
+    "cj_kernel_records": (C.c_int, [_P, C.c_int, C.POINTER(C.c_char_p), C.POINTER(C.c_float),
+                                    _U64P, C.POINTER(C.c_int)]),
+    "cj_copy": (C.c_int, [_P, _P, _P, C.c_uint64, C.c_int]),
+    "cj_scratch_peak": (C.c_uint64, [_P, C.c_int]),
     "cj_gen_pk_fk": (C.c_int, [_P, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
                                C.c_uint32, C.c_double, C.c_double, C.c_uint64, _P, _PP, _P, _PP]),
 }

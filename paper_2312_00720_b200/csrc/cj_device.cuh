@@ -102,5 +102,146 @@ __device__ __forceinline__ uint64_t warp_lookback(uint64_t* status, uint64_t idx
   return excl;
 }
 
+// SplitMix64 finaliser (the reference's rng.hpp:8-12), used as the shard hash.
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+// Digit of a key: bits [shift, shift + log2(mask+1)) or, when hparts > 0, the
+// shard of the key, floor(mix64(key) * hparts / 2^64) — uncorrelated with the
+// low key bits that pick partitions and hash slots.
+template <class K>
+__device__ __forceinline__ uint32_t key_digit(K k, uint32_t shift, uint32_t mask, uint32_t hparts) {
+  if (hparts) return (uint32_t)__umul64hi(mix64((uint64_t)k), (uint64_t)hparts);
+  return (uint32_t)(k >> shift) & mask;
+}
+
+// ---- TMA bulk copies (cp.async.bulk) + mbarrier ----------------------------
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// order earlier generic-proxy shared accesses before later async-proxy (TMA) writes
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_addr(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+// 1-D bulk copy global -> shared; 16-byte aligned addresses, size % 16 == 0.
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+// Stable in-warp peers of an 8-bit (or narrower) digit by bit ballots: the
+// lanes holding the same digit, restricted to `valid` lanes.
+__device__ __forceinline__ uint32_t digit_peers(uint32_t d, uint32_t bits, uint32_t valid) {
+  uint32_t peers = valid;
+#pragma unroll
+  for (uint32_t b = 0; b < 8; ++b) {
+    if (b < bits) {
+      const bool set = (d >> b) & 1u;
+      const uint32_t bal = __ballot_sync(0xffffffffu, set);
+      peers &= set ? bal : ~bal;
+    }
+  }
+  return peers;
+}
+
+// Exclusive scan of n u64 counts in three small launches (block scans, a scan
+// of the block totals, fix-up); no inter-block waiting.
+constexpr int kScanThreads = 512, kScanItems = 8, kScanTile = kScanThreads * kScanItems;
+
+template <int = 0>
+__global__ void __launch_bounds__(kScanThreads) k_scan_tiles(const uint64_t* __restrict__ in,
+                                                             uint64_t n, uint64_t* __restrict__ out,
+                                                             uint64_t* __restrict__ tile_tot) {
+  __shared__ uint64_t wsum[kScanThreads / 32];
+  const uint64_t base = (uint64_t)blockIdx.x * kScanTile + (uint64_t)threadIdx.x * kScanItems;
+  uint64_t v[kScanItems], local = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    v[i] = base + i < n ? in[base + i] : 0;
+    local += v[i];
+  }
+  const uint64_t inc = warp_inclusive_sum(local);
+  if ((threadIdx.x & 31) == 31) wsum[threadIdx.x >> 5] = inc;
+  __syncthreads();
+  uint64_t off = 0;
+  for (unsigned w = 0; w < (threadIdx.x >> 5); ++w) off += wsum[w];
+  uint64_t run = off + inc - local;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    if (base + i < n) out[base + i] = run;
+    run += v[i];
+  }
+  if (threadIdx.x == kScanThreads - 1) tile_tot[blockIdx.x] = run;
+}
+
+template <int = 0>
+__global__ void __launch_bounds__(1024) k_scan_top(uint64_t* __restrict__ tot, uint64_t ntiles,
+                                                    uint64_t* __restrict__ total) {
+  __shared__ uint64_t wsum[32];
+  const uint64_t per = (ntiles + blockDim.x - 1) / blockDim.x;
+  const uint64_t i0 = umin64(ntiles, threadIdx.x * per), i1 = umin64(ntiles, i0 + per);
+  uint64_t local = 0;
+  for (uint64_t i = i0; i < i1; ++i) local += tot[i];
+  const uint64_t inc = warp_inclusive_sum(local);
+  if ((threadIdx.x & 31) == 31) wsum[threadIdx.x >> 5] = inc;
+  __syncthreads();
+  uint64_t off = 0;
+  for (unsigned w = 0; w < (threadIdx.x >> 5); ++w) off += wsum[w];
+  uint64_t run = off + inc - local;
+  for (uint64_t i = i0; i < i1; ++i) {
+    const uint64_t t = tot[i];
+    tot[i] = run;
+    run += t;
+  }
+  if (threadIdx.x == blockDim.x - 1) *total = run;
+}
+
+template <int = 0>
+__global__ void k_scan_fix(uint64_t* __restrict__ out, uint64_t n,
+                           const uint64_t* __restrict__ tile_off) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] += tile_off[i / kScanTile];
+}
+
+// 16-byte aligned superset of an element range, for bulk copies of w-byte elements
+__device__ __forceinline__ uint64_t align_lo(uint64_t i, uint32_t w) { return i & ~(uint64_t)(16 / w - 1); }
+__device__ __forceinline__ uint64_t align_hi(uint64_t i, uint32_t w) {
+  return (i + 16 / w - 1) & ~(uint64_t)(16 / w - 1);
+}
+
 }  // namespace dev
 }  // namespace cj

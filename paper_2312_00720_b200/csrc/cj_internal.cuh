@@ -33,6 +33,7 @@ struct cj_ctx {
   bool own_stream = false;
   uint16_t epoch = 0;             // look-back status generation (see radix.cu)
   uint64_t launches = 0;          // kernels launched through this ctx
+  uint64_t scratch_now = 0, scratch_peak = 0;  // device scratch held by operators
   std::string last_error;
   // persistent scratch (grown on demand, never shrunk)
   uint64_t* status = nullptr;     // decoupled look-back words
@@ -70,8 +71,15 @@ namespace cj {
 struct Scratch {
   cj_ctx* ctx;
   void* p = nullptr;
-  Scratch(cj_ctx* c, uint64_t bytes) : ctx(c), p(c->alloc(bytes ? bytes : 16)) {}
-  ~Scratch() { if (p) ctx->release(p); }
+  uint64_t n = 0;
+  Scratch(cj_ctx* c, uint64_t bytes) : ctx(c), p(c->alloc(bytes ? bytes : 16)), n(bytes) {
+    c->scratch_now += n;
+    if (c->scratch_now > c->scratch_peak) c->scratch_peak = c->scratch_now;
+  }
+  ~Scratch() {
+    if (p) ctx->release(p);
+    ctx->scratch_now -= n;
+  }
   Scratch(const Scratch&) = delete;
   Scratch& operator=(const Scratch&) = delete;
   template <class T> T* as() const { return static_cast<T*>(p); }
@@ -91,16 +99,45 @@ struct PassPlan {
   uint32_t lo[64] = {}, hi[64] = {};
 };
 
-// Digit counts of every pass in one read of the keys; counts_dev[p*256 + d].
-// Also writes the exclusive digit bases base_dev[p*256+d] (u64) and returns
-// which passes are live (not constant) after one host round trip.
-void histogram_passes(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes,
-                      const PassPlan& plan, uint32_t* counts_dev, uint64_t* base_dev,
-                      std::vector<uint32_t>* counts_host);
+// Geometry of a blocked scatter pass: tile size (shared-memory budget), tile
+// count, one static block of consecutive tiles per CTA, stage layout.
+struct ScatterGeom {
+  int items = 8;
+  uint64_t tile = 4096, tiles = 1;
+  uint32_t nblocks = 1;
+  size_t smem = 0;
+  uint32_t stage_bytes = 0, pbytes = 0;
+  uint32_t voff[CJ_MAX_COLS + 1] = {};
+  bool tma = false;  // all inputs 16-byte aligned (TMA bulk copies)
+  int ctas_per_sm = 2, stages = 2;
+};
+ScatterGeom scatter_geom(cj_ctx* ctx, uint64_t n, int key_bytes, const ValCols& vals,
+                         const void* keys_in);
 
-// One stable scatter pass (onesweep; decoupled look-back across tiles).
+// Per-block digit counts (cnt[b][p][256]) of every pass of `plan` (<= 8) in one
+// read of the keys, over the blocks of geometry g.
+void block_hist(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes, const PassPlan& plan,
+                const ScatterGeom& g, uint32_t* cnt_dev, uint32_t hparts = 0);
+
+// block_hist + digit totals (totals_dev[p*256+d]) + exclusive digit bases
+// (base_dev[p*256+d]); totals_host after one host round trip when non-null.
+void histogram_passes(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes,
+                      const PassPlan& plan, const ScatterGeom& g, uint32_t* cnt_dev,
+                      uint32_t* totals_dev, uint64_t* base_dev,
+                      std::vector<uint32_t>* totals_host, uint32_t hparts = 0);
+
+// One stable scatter pass.  With per-block counts of this pass (cnt, stride
+// cnt_stride) and a TMA-eligible geometry it runs the blocked kernel (no
+// inter-CTA waiting); otherwise the onesweep kernel with decoupled look-back.
 void scatter_pass(cj_ctx* ctx, const void* keys_in, void* keys_out, uint64_t n, int key_bytes,
-                  uint32_t lo, uint32_t hi, const uint64_t* base_dev, const ValCols& vals);
+                  uint32_t lo, uint32_t hi, const uint64_t* base_dev, const uint32_t* cnt,
+                  uint32_t cnt_stride, const ScatterGeom& g, const ValCols& vals,
+                  uint32_t hparts = 0);
+
+// Stable partition of rows by shard = floor(mix64(key) * parts / 2^64) (the
+// multi-GPU shuffle's send layout); counts_host[parts] rows per shard.
+void shard_partition(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, int key_bytes,
+                     uint32_t parts, const ValCols& vals, uint64_t* counts_host);
 
 // Stable LSD over the plan; constant-digit passes skipped; the last executed
 // pass lands in the caller's outputs.  gen_ids handled in the first pass.
@@ -134,7 +171,13 @@ struct OutSpec {
   void* s_dst[CJ_MAX_COLS] = {};
   uint32_t r_bytes[CJ_MAX_COLS] = {};
   uint32_t s_bytes[CJ_MAX_COLS] = {};
+  bool padded = false;             // keys + src columns readable 16 B past the end (TMA path)
+  uint64_t r_rows = 0, s_rows = 0; // input sizes (timing records only)
 };
+
+// Allocation slack that keeps 16-byte-aligned bulk copies of any row range
+// inside the allocation.
+constexpr uint64_t kPad = 64;
 
 // hash_join.cu: partitioned hash join (count + look-back + fill), outputs per
 // OutSpec; capacity = rows the outputs can hold (CJ_ERR_CAPACITY_EXCEEDED
@@ -162,6 +205,13 @@ uint64_t nphj_find(cj_ctx* ctx, const void* rkeys, uint64_t nr, const void* skey
 void gen_pk_fk(cj_ctx* ctx, uint64_t r_rows, uint64_t s_rows, uint32_t r_pay, uint32_t s_pay,
                uint32_t key_bytes, uint32_t pay_bytes, double match_ratio, double zipf,
                uint64_t seed, void* r_key, void* const* r_pays, void* s_key, void* const* s_pays);
+
+// Exclusive scan of n u64 counts on the ctx stream; *total_dev = sum.
+void scan_counts(cj_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* out, uint64_t* total_dev);
+
+void gen_shard(cj_ctx* ctx, uint64_t r_total, uint64_t s_total, uint32_t rank, uint32_t ranks,
+               uint32_t r_pay, uint32_t s_pay, uint64_t seed, void* r_key, void* const* r_pays,
+               void* s_key, void* const* s_pays);
 
 // error word helpers: kernels OR codes into ctx->err_word; raise after sync
 enum : uint32_t { kErrOOB = 1u, kErrOverflow = 2u, kErrNotSorted = 4u, kErrDupKeys = 8u };

@@ -40,6 +40,21 @@ void check_cuda(cudaError_t e, const char* what) {
   }
 }
 
+void scan_counts(cj_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* out, uint64_t* total_dev) {
+  const uint64_t tiles = std::max<uint64_t>((n + dev::kScanTile - 1) / dev::kScanTile, 1);
+  Scratch tot(ctx, tiles * 8);
+  ctx->kbegin("scan", n * 16);
+  dev::k_scan_tiles<0><<<(unsigned)tiles, dev::kScanThreads, 0, ctx->stream>>>(in, n, out,
+                                                                               tot.as<uint64_t>());
+  dev::k_scan_top<0><<<1, 1024, 0, ctx->stream>>>(tot.as<uint64_t>(), tiles, total_dev);
+  if (n > 0)
+    dev::k_scan_fix<0><<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(out, n,
+                                                                            tot.as<uint64_t>());
+  ctx->kend();
+  ctx->launches += 2;
+  CJ_CUDA(cudaGetLastError());
+}
+
 void raise_device_errors(cj_ctx* ctx) {
   CJ_CUDA(cudaMemcpyAsync(ctx->host_pinned + 64, ctx->err_word, sizeof(uint32_t),
                           cudaMemcpyDeviceToHost, ctx->stream));
@@ -173,7 +188,7 @@ Side transform(cj_ctx* ctx, const cj_relation* rel, int algo, bool gfur, unsigne
   Side s;
   const uint64_t n = rel->rows;
   const int kb = (int)rel->key_bytes;
-  s.keys = ctx->alloc(std::max<uint64_t>(n * kb, 16));
+  s.keys = ctx->alloc(n * kb + kPad);
   owned.push_back(s.keys);
   ValCols v;
   if (gfur) {
@@ -181,14 +196,14 @@ Side transform(cj_ctx* ctx, const cj_relation* rel, int algo, bool gfur, unsigne
     v.gen_ids = 1;
     v.in[0] = nullptr;
     v.bytes[0] = 4;
-    v.out[0] = ctx->alloc(std::max<uint64_t>(n * 4, 16));
+    v.out[0] = ctx->alloc(n * 4 + kPad);
     owned.push_back(v.out[0]);
   } else {
     v.n = (int)rel->npay;
     for (uint32_t c = 0; c < rel->npay; ++c) {
       v.in[c] = rel->pay[c];
       v.bytes[c] = rel->pay_bytes[c];
-      v.out[c] = ctx->alloc(std::max<uint64_t>(n * rel->pay_bytes[c], 16));
+      v.out[c] = ctx->alloc(n * rel->pay_bytes[c] + kPad);
       owned.push_back(v.out[c]);
     }
   }
@@ -363,6 +378,9 @@ void run_join_dev(cj_ctx* ctx, const cj_relation* R, const cj_relation* S,
     o.key = res->key;
     o.ids_r = res->ids_r;
     o.ids_s = res->ids_s;
+    o.padded = true;  // transformed columns carry kPad bytes of slack
+    o.r_rows = R->rows;
+    o.s_rows = S->rows;
     if (gfur) {
       o.ids_r = res->ids_r ? res->ids_r : nullptr;
       o.carried_r = static_cast<const uint32_t*>(tr.cols[0]);
@@ -604,6 +622,24 @@ int cj_alloc(cj_ctx* ctx, uint64_t bytes, void** p) {
 
 uint64_t cj_launch_count(const cj_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+uint64_t cj_scratch_peak(cj_ctx* ctx, int reset) {
+  if (!ctx) return 0;
+  const uint64_t p = ctx->scratch_peak;
+  if (reset) ctx->scratch_peak = ctx->scratch_now;
+  return p;
+}
+
+int cj_copy(cj_ctx* ctx, void* dst, const void* src, uint64_t bytes, int kind) {
+  return cj::guarded(ctx, [&] {
+    if (bytes == 0) return;
+    const cudaMemcpyKind k = kind == 1   ? cudaMemcpyHostToDevice
+                             : kind == 2 ? cudaMemcpyDeviceToHost
+                                         : cudaMemcpyDeviceToDevice;
+    CJ_CUDA(cudaMemcpyAsync(dst, src, bytes, k, ctx->stream));
+    if (kind != 3) CJ_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
 int cj_mark(cj_ctx* ctx, int slot) {
   return cj::guarded(ctx, [&] {
     if (slot < 0 || slot >= 16) cj::fail(CJ_ERR_SPEC_INVALID, "mark slot out of range");
@@ -652,9 +688,13 @@ int cj_histogram(cj_ctx* ctx, const void* keys, uint64_t n, uint32_t kb, uint32_
     plan.npasses = 1;
     plan.lo[0] = lo;
     plan.hi[0] = hi;
-    cj::Scratch cnt(ctx, 4 * cj::kRadix), base(ctx, 8 * cj::kRadix);
+    cj::ValCols none;
+    const cj::ScatterGeom g = cj::scatter_geom(ctx, n, (int)kb, none, keys);
+    cj::Scratch cnt(ctx, 4ull * cj::kRadix * g.nblocks), tot(ctx, 4 * cj::kRadix),
+        base(ctx, 8 * cj::kRadix);
     std::vector<uint32_t> h;
-    cj::histogram_passes(ctx, keys, n, (int)kb, plan, cnt.as<uint32_t>(), base.as<uint64_t>(), &h);
+    cj::histogram_passes(ctx, keys, n, (int)kb, plan, g, cnt.as<uint32_t>(), tot.as<uint32_t>(),
+                         base.as<uint64_t>(), &h);
     std::memcpy(counts_host, h.data(), sizeof(uint32_t) * (1u << (hi - lo)));
   });
 }
@@ -696,10 +736,14 @@ int cj_radix_partition(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n
     plan.npasses = 1;
     plan.lo[0] = lo;
     plan.hi[0] = hi;
-    cj::Scratch cnt(ctx, 4 * cj::kRadix), base(ctx, 8 * cj::kRadix);
+    const cj::ScatterGeom g = cj::scatter_geom(ctx, n, (int)kb, v, keys);
+    cj::Scratch cnt(ctx, 4ull * cj::kRadix * g.nblocks), tot(ctx, 4 * cj::kRadix),
+        base(ctx, 8 * cj::kRadix);
     std::vector<uint32_t> h;
-    cj::histogram_passes(ctx, keys, n, (int)kb, plan, cnt.as<uint32_t>(), base.as<uint64_t>(), &h);
-    cj::scatter_pass(ctx, keys, keys_out, n, (int)kb, lo, hi, base.as<uint64_t>(), v);
+    cj::histogram_passes(ctx, keys, n, (int)kb, plan, g, cnt.as<uint32_t>(), tot.as<uint32_t>(),
+                         base.as<uint64_t>(), &h);
+    cj::scatter_pass(ctx, keys, keys_out, n, (int)kb, lo, hi, base.as<uint64_t>(),
+                     cnt.as<uint32_t>(), cj::kRadix, g, v);
     if (offsets_host) {
       const uint32_t fan = 1u << (hi - lo);
       offsets_host[0] = 0;
@@ -715,7 +759,7 @@ int cj_radix_partition_passes(cj_ctx* ctx, const void* keys, void* keys_out, uin
                               const uint32_t* vbytes, uint32_t nvals, int gen_ids) {
   return cj::guarded(ctx, [&] {
     cj::check_key_bytes(kb);
-    if (npasses > CJ_MAX_PASSES) cj::fail(CJ_ERR_UNSUPPORTED, "plan longer than 8 passes");
+    if (npasses > 64) cj::fail(CJ_ERR_UNSUPPORTED, "plan longer than 64 passes");
     cj::PassPlan plan;
     plan.npasses = (int)npasses;
     for (uint32_t p = 0; p < npasses; ++p) {
@@ -726,7 +770,7 @@ int cj_radix_partition_passes(cj_ctx* ctx, const void* keys, void* keys_out, uin
       plan.hi[p] = plan_hi[p];
     }
     cj::ValCols v = make_vals(vin, vout, vbytes, nvals, gen_ids);
-    cj::lsd_partition(ctx, keys, keys_out, n, (int)kb, plan, v);
+    cj::lsd_any(ctx, keys, keys_out, n, (int)kb, plan, v);
     CJ_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
@@ -917,6 +961,25 @@ int cj_run_join_host(cj_ctx* ctx, const cj_relation* build, const cj_relation* p
     CJ_CUDA(cudaStreamSynchronize(ctx->stream));
     if (h2d_ns) *h2d_ns = tm.ns(0, 1);
     if (d2h_ns) *d2h_ns = tm.ns(2, 3);
+  });
+}
+
+int cj_shard_partition(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, uint32_t kb,
+                       uint32_t parts, const void* const* vin, void* const* vout,
+                       const uint32_t* vbytes, uint32_t nvals, uint64_t* counts_host) {
+  return cj::guarded(ctx, [&] {
+    cj::check_key_bytes(kb);
+    cj::ValCols v = make_vals(vin, vout, vbytes, nvals, 0);
+    cj::shard_partition(ctx, keys, keys_out, n, (int)kb, parts, v, counts_host);
+  });
+}
+
+int cj_gen_shard(cj_ctx* ctx, uint64_t r_total, uint64_t s_total, uint32_t rank, uint32_t ranks,
+                 uint32_t r_pay, uint32_t s_pay, uint64_t seed, void* r_key, void* const* r_pays,
+                 void* s_key, void* const* s_pays) {
+  return cj::guarded(ctx, [&] {
+    cj::gen_shard(ctx, r_total, s_total, rank, ranks, r_pay, s_pay, seed, r_key, r_pays, s_key,
+                  s_pays);
   });
 }
 

@@ -11,6 +11,7 @@
 #include <cmath>
 #include <vector>
 
+#include "cj_device.cuh"
 #include "cj_internal.cuh"
 
 namespace cj {
@@ -18,11 +19,7 @@ namespace {
 
 constexpr uint64_t kGold = 0x9E3779B97F4A7C15ull;
 
-__host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
-  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
-  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
-  return x ^ (x >> 31);
-}
+using dev::mix64;
 __host__ __device__ __forceinline__ uint64_t stream_of(uint64_t seed, uint64_t tag) {
   return mix64(seed ^ mix64(tag + kGold));
 }
@@ -91,7 +88,70 @@ __global__ void k_payload(uint64_t seed, uint64_t n, T* out) {
     out[i] = (T)rng_at(seed, i);
 }
 
+// Bijection of [0, 2^m): rounds of (odd multiply, add, xor-shift), all mod 2^m.
+__device__ __forceinline__ uint64_t scramble(uint64_t x, uint32_t m, uint64_t seed) {
+  const uint64_t mask = m >= 64 ? ~0ull : ((1ull << m) - 1);
+  const uint32_t sh = m > 1 ? (m + 1) / 2 : 1;
+  uint64_t k = seed;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    k = mix64(k + kGold);
+    x = (x * (k | 1ull) + (k >> 7)) & mask;
+    x ^= x >> sh;
+  }
+  return x;
+}
+
+__global__ void k_shard(uint64_t r_total, uint32_t m, uint64_t s_total, uint64_t r_lo, uint64_t r_n,
+                        uint64_t s_lo, uint64_t s_n, uint64_t seed, uint32_t* __restrict__ rk,
+                        uint32_t* __restrict__ sk) {
+  const uint64_t pseed = stream_of(seed, 0x52100000ull), fseed = stream_of(seed, 0x53100000ull);
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < r_n; i += stride)
+    rk[i] = (uint32_t)scramble(r_lo + i, m, pseed);
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < s_n; j += stride)
+    sk[j] = (uint32_t)__umul64hi(rng_at(fseed, s_lo + j), r_total);
+}
+
+template <class T>
+__global__ void k_payload_at(uint64_t seed, uint64_t first, uint64_t n, T* out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = (T)rng_at(seed, first + i);
+}
+
 }  // namespace
+
+void gen_shard(cj_ctx* ctx, uint64_t r_total, uint64_t s_total, uint32_t rank, uint32_t ranks,
+               uint32_t r_pay, uint32_t s_pay, uint64_t seed, void* r_key, void* const* r_pays,
+               void* s_key, void* const* s_pays) {
+  if (ranks == 0 || rank >= ranks) fail(CJ_ERR_SPEC_INVALID, "rank out of range");
+  if (r_total == 0 || (r_total & (r_total - 1)) || r_total % ranks || s_total % ranks)
+    fail(CJ_ERR_SPEC_INVALID, "shard generator needs |R| a power of two and |R|,|S| divisible by ranks");
+  if (r_total > (1ull << 32)) fail(CJ_ERR_UNSUPPORTED, "shard generator keys are 4 bytes");
+  uint32_t m = 0;
+  while ((1ull << m) < r_total) ++m;
+  const uint64_t rn = r_total / ranks, sn = s_total / ranks, r_lo = rn * rank, s_lo = sn * rank;
+  const unsigned grid = ctx->num_sms * 8;
+  ctx->kbegin("gen_shard", 4 * (rn + sn));
+  k_shard<<<grid, 256, 0, ctx->stream>>>(r_total, m, s_total, r_lo, rn, s_lo, sn, seed,
+                                         static_cast<uint32_t*>(r_key), static_cast<uint32_t*>(s_key));
+  ctx->kend();
+  for (uint32_t c = 0; c < r_pay; ++c) {
+    ctx->kbegin("gen_payload", rn * 4);
+    k_payload_at<uint32_t><<<grid, 256, 0, ctx->stream>>>(stream_of(seed, 0x7000ull + c), r_lo, rn,
+                                                          static_cast<uint32_t*>(r_pays[c]));
+    ctx->kend();
+  }
+  for (uint32_t c = 0; c < s_pay; ++c) {
+    ctx->kbegin("gen_payload", sn * 4);
+    k_payload_at<uint32_t><<<grid, 256, 0, ctx->stream>>>(stream_of(seed, 0x8000ull + c), s_lo, sn,
+                                                          static_cast<uint32_t*>(s_pays[c]));
+    ctx->kend();
+  }
+  CJ_CUDA(cudaGetLastError());
+  CJ_CUDA(cudaStreamSynchronize(ctx->stream));
+}
 
 void gen_pk_fk(cj_ctx* ctx, uint64_t r_rows, uint64_t s_rows, uint32_t r_pay, uint32_t s_pay,
                uint32_t key_bytes, uint32_t pay_bytes, double match_ratio, double zipf,

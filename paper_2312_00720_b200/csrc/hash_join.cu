@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "cj_device.cuh"
@@ -31,56 +32,85 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr uint32_t kProbeChunk = 4096;
+// Probe rows per work unit; the unit sequence (partition, build chunk, probe
+// chunk) concatenates to the reference's emission order for any chunk size.
+uint32_t probe_chunk() {
+  const char* e = std::getenv("CJ_QCHUNK");
+  return e ? (uint32_t)std::max(256, std::min(16384, std::atoi(e))) : 4096u;
+}
+int find_ctas_per_sm() {
+  const char* e = std::getenv("CJ_FIND_CTAS");
+  return e ? std::max(1, std::atoi(e)) : 1;
+}
+int find_stages() {
+  const char* e = std::getenv("CJ_FIND_STAGES");
+  return e ? std::min(2, std::max(1, std::atoi(e))) : 2;
+}
 constexpr uint16_t kEmpty16 = 0xffffu;
 constexpr uint32_t kNoMatch = 0xffffffffu;
 
-struct PlanArgs {
+// unit_start[p] = number of units before partition p (units with an empty
+// side produce no rows and are dropped).  Grid-wide: each block scans 1024
+// partitions and chains its total by decoupled look-back.
+constexpr int kPlanThreads = 256, kPlanPer = 4;
+
+struct PlanArgs2 {
   const uint64_t* boff;
   const uint64_t* poff;
   uint32_t fanout, limit, qchunk;
-  uint64_t* unit_start;   // fanout + 1
-  uint64_t* stats;        // [0] max build chunk, [1] total units
+  uint64_t* unit_start;     // fanout + 1
+  unsigned long long* stats;// [0] max build chunk (atomicMax), [1] total units
+  uint64_t* status;
+  uint64_t epoch;
+  uint32_t* err;
 };
 
-// unit_start[p] = number of units before partition p (units with an empty
-// side produce no rows and are dropped).
-__global__ void __launch_bounds__(1024) k_phj_plan(const PlanArgs a) {
-  __shared__ uint64_t wsum[32];
-  const uint32_t per = (a.fanout + blockDim.x - 1) / blockDim.x;
-  const uint32_t p0 = min(a.fanout, threadIdx.x * per), p1 = min(a.fanout, p0 + per);
+__global__ void __launch_bounds__(kPlanThreads) k_phj_plan(const __grid_constant__ PlanArgs2 a) {
+  __shared__ uint64_t wsum[kPlanThreads / 32];
+  __shared__ uint64_t s_base;
+  const uint32_t p0 = (blockIdx.x * kPlanThreads + threadIdx.x) * kPlanPer;
+  uint64_t cnt[kPlanPer];
   uint64_t local = 0, maxc = 0;
-  for (uint32_t p = p0; p < p1; ++p) {
-    const uint64_t nb = a.boff[p + 1] - a.boff[p], ns = a.poff[p + 1] - a.poff[p];
-    if (nb && ns) {
-      local += ((nb + a.limit - 1) / a.limit) * ((ns + a.qchunk - 1) / a.qchunk);
-      maxc = max(maxc, dev::umin64(nb, a.limit));
+#pragma unroll
+  for (int i = 0; i < kPlanPer; ++i) {
+    const uint32_t p = p0 + i;
+    cnt[i] = 0;
+    if (p < a.fanout) {
+      const uint64_t nb = a.boff[p + 1] - a.boff[p], ns = a.poff[p + 1] - a.poff[p];
+      if (nb && ns) {
+        cnt[i] = ((nb + a.limit - 1) / a.limit) * ((ns + a.qchunk - 1) / a.qchunk);
+        maxc = max(maxc, dev::umin64(nb, a.limit));
+      }
+    }
+    local += cnt[i];
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t inc = dev::warp_inclusive_sum(local);
+  if (lane == 31) wsum[warp] = inc;
+  for (int o = 16; o > 0; o >>= 1) maxc = max(maxc, __shfl_xor_sync(0xffffffffu, maxc, o));
+  if (lane == 0 && maxc) atomicMax(&a.stats[0], (unsigned long long)maxc);
+  __syncthreads();
+  if (warp == 0) {
+    uint64_t v = lane < kPlanThreads / 32 ? wsum[lane] : 0;
+    const uint64_t tot = dev::warp_sum(v);
+    const uint64_t base = dev::warp_lookback(a.status, blockIdx.x, tot, a.epoch, a.err);
+    if (lane == 0) {
+      s_base = base;
+      if (blockIdx.x == gridDim.x - 1) {
+        a.unit_start[a.fanout] = base + tot;
+        a.stats[1] = base + tot;
+      }
     }
   }
-  const uint64_t inc = dev::warp_inclusive_sum(local);
-  if ((threadIdx.x & 31) == 31) wsum[threadIdx.x >> 5] = inc;
   __syncthreads();
-  uint64_t off = 0;
-  for (unsigned w = 0; w < (threadIdx.x >> 5); ++w) off += wsum[w];
+  uint64_t off = s_base;
+  for (int w = 0; w < warp; ++w) off += wsum[w];
   uint64_t run = off + inc - local;
-  for (uint32_t p = p0; p < p1; ++p) {
-    a.unit_start[p] = run;
-    const uint64_t nb = a.boff[p + 1] - a.boff[p], ns = a.poff[p + 1] - a.poff[p];
-    if (nb && ns) run += ((nb + a.limit - 1) / a.limit) * ((ns + a.qchunk - 1) / a.qchunk);
-  }
-  if (threadIdx.x == blockDim.x - 1) {
-    a.unit_start[a.fanout] = run;
-    a.stats[1] = run;
-  }
-  // block max of chunk sizes
-  for (int o = 16; o > 0; o >>= 1) maxc = max(maxc, __shfl_xor_sync(0xffffffffu, maxc, o));
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = maxc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint64_t m = 0;
-    for (unsigned w = 0; w < blockDim.x / 32; ++w) m = max(m, wsum[w]);
-    a.stats[0] = m;
+#pragma unroll
+  for (int i = 0; i < kPlanPer; ++i) {
+    const uint32_t p = p0 + i;
+    if (p < a.fanout) a.unit_start[p] = run;
+    run += cnt[i];
   }
 }
 
@@ -113,6 +143,16 @@ struct FindArgs {
   uint32_t r_bytes[CJ_MAX_COLS];
   uint32_t s_bytes[CJ_MAX_COLS];
   uint32_t r_stage_off[CJ_MAX_COLS];  // byte offsets of staged columns
+  // TMA path: stage layout (byte offsets within one stage buffer)
+  uint32_t stage_bytes, off_bk, off_pk, cap_entries;
+  uint32_t off_r[CJ_MAX_COLS], off_s[CJ_MAX_COLS];
+  int padded;  // every staged array is readable 16 bytes past its end
+  // count / fill passes
+  const void* desc;          // UnitDesc[n_units]
+  uint64_t n_units;
+  uint64_t* unit_off;        // exclusive output offset per unit (fill)
+  uint64_t nb_rows, np_rows; // sizes of the partitioned inputs
+  int stages;                // 2: prefetch the next unit while this one runs
 };
 
 template <class K>
@@ -345,6 +385,269 @@ __global__ void __launch_bounds__(kThreads) k_phj_find(const __grid_constant__ F
   }
 }
 
+// ---- TMA-pipelined count / fill (the default for run_join) -------------------
+//
+// No inter-CTA waiting: a count pass writes every unit's match count, a scan
+// turns them into output offsets, and the fill pass writes each unit's rows at
+// its offset.  Both passes are persistent (one CTA of 512 threads per SM, unit
+// u_k = blockIdx + k * gridDim) and double-buffered: a unit's build chunk (keys
+// + transformed R payload slices) and probe chunk (keys + transformed S payload
+// slices) are contiguous ranges, bulk-copied (cp.async.bulk, 16-byte aligned
+// supersets of the ranges) into one shared-memory stage while the previous
+// unit is built, probed and written from the other.  Unit descriptors are
+// precomputed, so the next unit's copies are issued without a dependent lookup.
+constexpr int kTmaThreads = 512;
+constexpr int kTmaWarps = kTmaThreads / 32;
+
+struct UnitDesc {
+  uint64_t b_lo, b_hi, q_lo, q_hi;
+};
+
+__global__ void k_phj_desc(const uint64_t* __restrict__ boff, const uint64_t* __restrict__ poff,
+                           const uint64_t* __restrict__ unit_start, uint32_t fanout,
+                           uint32_t limit, uint32_t qchunk, UnitDesc* __restrict__ desc) {
+  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < fanout; p += gridDim.x * blockDim.x) {
+    const uint64_t u0 = unit_start[p], u1 = unit_start[p + 1];
+    if (u0 == u1) continue;
+    const uint64_t b0 = boff[p], b1 = boff[p + 1], q0 = poff[p], q1 = poff[p + 1];
+    const uint64_t nqc = (q1 - q0 + qchunk - 1) / qchunk;
+    for (uint64_t l = 0; l < u1 - u0; ++l) {
+      UnitDesc d;
+      d.b_lo = b0 + (l / nqc) * limit;
+      d.b_hi = dev::umin64(b1, d.b_lo + limit);
+      d.q_lo = q0 + (l % nqc) * qchunk;
+      d.q_hi = dev::umin64(q1, d.q_lo + qchunk);
+      desc[u0 + l] = d;
+    }
+  }
+}
+
+template <class K, bool WRITE>
+__global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constant__ FindArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint16_t* tab = reinterpret_cast<uint16_t*>(smem + (size_t)a.stages * a.stage_bytes);
+  uint32_t* res = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(tab) + 2 * (size_t)a.cap_entries);
+  __shared__ UnitDesc s_desc[2];
+  __shared__ __align__(8) uint64_t mbar[2];
+  __shared__ uint64_t s_wcount[kTmaWarps], s_wbase[kTmaWarps];
+  __shared__ int s_dup;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t units = a.n_units;
+  const UnitDesc* __restrict__ descs = reinterpret_cast<const UnitDesc*>(a.desc);
+  const uint32_t kb = sizeof(K);
+
+  auto bytes = [&](uint64_t lo, uint64_t hi, uint32_t w) {
+    return (uint32_t)((dev::align_hi(hi, w) - dev::align_lo(lo, w)) * w);
+  };
+  auto issue = [&](int b, const UnitDesc& d) {  // thread 0
+    uint8_t* st = smem + (size_t)b * a.stage_bytes;
+    uint32_t total = bytes(d.b_lo, d.b_hi, kb) + bytes(d.q_lo, d.q_hi, kb);
+    if (WRITE) {
+      for (int c = 0; c < a.nr; ++c) total += bytes(d.b_lo, d.b_hi, a.r_bytes[c]);
+      for (int c = 0; c < a.ns; ++c) total += bytes(d.q_lo, d.q_hi, a.s_bytes[c]);
+    }
+    dev::mbar_expect_tx(&mbar[b], total);
+    auto copy = [&](uint32_t off, const void* base, uint64_t lo, uint64_t hi, uint32_t w) {
+      dev::tma_load_1d(st + off, static_cast<const uint8_t*>(base) + dev::align_lo(lo, w) * w,
+                       bytes(lo, hi, w), &mbar[b]);
+    };
+    copy(a.off_bk, a.bkeys, d.b_lo, d.b_hi, kb);
+    copy(a.off_pk, a.pkeys, d.q_lo, d.q_hi, kb);
+    if (WRITE) {
+      for (int c = 0; c < a.nr; ++c) copy(a.off_r[c], a.r_src[c], d.b_lo, d.b_hi, a.r_bytes[c]);
+      for (int c = 0; c < a.ns; ++c) copy(a.off_s[c], a.s_src[c], d.q_lo, d.q_hi, a.s_bytes[c]);
+    }
+  };
+
+  uint64_t u = blockIdx.x;
+  UnitDesc next{};  // descriptor of the unit after the one in flight (thread 0)
+  if (tid == 0) {
+    dev::mbar_init(&mbar[0], 1);
+    dev::mbar_init(&mbar[1], 1);
+    dev::fence_mbar_init();
+    if (u < units) {
+      s_desc[0] = descs[u];
+      issue(0, s_desc[0]);
+    }
+    if (u + gridDim.x < units) next = descs[u + gridDim.x];
+  }
+  __syncthreads();
+  uint32_t phase[2] = {0, 0};
+  int b = 0;
+  auto issue_next = [&](int nb_) {  // thread 0: copies of unit u + gridDim.x into stage nb_
+    if (u + gridDim.x < units) {
+      s_desc[nb_] = next;
+      dev::fence_proxy_async();
+      issue(nb_, next);
+      if (u + 2ull * gridDim.x < units) next = descs[u + 2ull * gridDim.x];  // in flight
+    }
+  };
+  for (; u < units; u += gridDim.x, b = (b + 1) % a.stages) {
+    const UnitDesc inf = s_desc[b];
+    if (tid == 0) {
+      if (a.stages == 2) issue_next(b ^ 1);
+      s_dup = 0;
+    }
+    uint64_t unit_base = 0;
+    if (WRITE && tid == 32) unit_base = a.unit_off[u];
+    const uint32_t nb = (uint32_t)(inf.b_hi - inf.b_lo), nq = (uint32_t)(inf.q_hi - inf.q_lo);
+    uint32_t cap_log2 = 1;
+    while ((1u << cap_log2) < 2 * nb) ++cap_log2;
+    const uint32_t cap = 1u << cap_log2, cmask = cap - 1;
+    for (uint32_t i = tid; i < cap; i += kTmaThreads) tab[i] = kEmpty16;
+    uint8_t* st = smem + (size_t)b * a.stage_bytes;
+    const K* bk = reinterpret_cast<const K*>(st + a.off_bk) + (inf.b_lo - dev::align_lo(inf.b_lo, kb));
+    const K* pk = reinterpret_cast<const K*>(st + a.off_pk) + (inf.q_lo - dev::align_lo(inf.q_lo, kb));
+    dev::mbar_wait(&mbar[b], phase[b]);
+    phase[b] ^= 1;
+    __syncthreads();
+
+    // 1. insert chunk positions (CAS); meeting an equal key marks duplicates
+    bool dup = false;
+    for (uint32_t i = tid; i < nb; i += kTmaThreads) {
+      const K k = bk[i];
+      uint32_t sl = slot_of(k, cap_log2);
+      while (true) {
+        const uint16_t old = atomicCAS(&tab[sl], kEmpty16, (uint16_t)i);
+        if (old == kEmpty16) break;
+        if (bk[old] == k) dup = true;
+        sl = (sl + 1) & cmask;
+      }
+    }
+    if (__syncthreads_or(dup)) s_dup = 1;
+    __syncthreads();
+    const bool has_dup = s_dup != 0;
+    uint16_t* sidx = tab;
+    if (has_dup) {  // stably sorted chunk positions: bitonic over (key, position)
+      uint32_t np2 = 1;
+      while (np2 < nb) np2 <<= 1;
+      for (uint32_t i = tid; i < np2; i += kTmaThreads) sidx[i] = i < nb ? (uint16_t)i : kEmpty16;
+      __syncthreads();
+      for (uint32_t kk = 2; kk <= np2; kk <<= 1) {
+        for (uint32_t jj = kk >> 1; jj > 0; jj >>= 1) {
+          for (uint32_t i = tid; i < np2; i += kTmaThreads) {
+            const uint32_t l = i ^ jj;
+            if (l > i) {
+              const uint16_t x = sidx[i], y = sidx[l];
+              bool gt;
+              if (x == kEmpty16) gt = y != kEmpty16;
+              else if (y == kEmpty16) gt = false;
+              else gt = bk[x] > bk[y] || (bk[x] == bk[y] && x > y);
+              if (gt == ((i & kk) == 0)) { sidx[i] = y; sidx[l] = x; }
+            }
+          }
+          __syncthreads();
+        }
+      }
+    }
+
+    // 2. probe from shared memory; warp w owns a contiguous run of rounds
+    const uint32_t rounds = (nq + 31) / 32;
+    const uint32_t r0 = (uint32_t)((uint64_t)rounds * warp / kTmaWarps);
+    const uint32_t r1 = (uint32_t)((uint64_t)rounds * (warp + 1) / kTmaWarps);
+    uint64_t wcount = 0;
+    for (uint32_t r = r0; r < r1; ++r) {
+      const uint32_t jl = r * 32 + lane;
+      if (jl < nq) {
+        const K k = pk[jl];
+        uint32_t out = kNoMatch, m = 0;
+        if (!has_dup) {
+          uint32_t sl = slot_of(k, cap_log2);
+          while (true) {
+            const uint16_t e = tab[sl];
+            if (e == kEmpty16) break;
+            if (bk[e] == k) { out = e; m = 1; break; }
+            sl = (sl + 1) & cmask;
+          }
+        } else {
+          uint32_t lo = 0, hi = nb;
+          while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (bk[sidx[mid]] < k) lo = mid + 1; else hi = mid;
+          }
+          uint32_t lo2 = lo, hi2 = nb;
+          while (lo2 < hi2) {
+            const uint32_t mid = (lo2 + hi2) >> 1;
+            if (bk[sidx[mid]] <= k) lo2 = mid + 1; else hi2 = mid;
+          }
+          m = lo2 - lo;
+          out = (lo << 16) | m;
+        }
+        if (WRITE) res[jl] = out;
+        wcount += m;
+      }
+    }
+    wcount = dev::warp_sum(wcount);
+    if (lane == 0) s_wcount[warp] = wcount;
+    __syncthreads();
+    if (warp == 1) {
+      const uint64_t wc = lane < kTmaWarps ? s_wcount[lane] : 0;
+      const uint64_t inc = dev::warp_inclusive_sum(wc);
+      const uint64_t base = __shfl_sync(0xffffffffu, unit_base, 0);
+      if (lane < kTmaWarps) s_wbase[lane] = base + inc - wc;
+      if (!WRITE && lane == kTmaWarps - 1) a.unit_counts[u] = inc;
+    }
+    if (!WRITE) {
+      // two stages: shared state is rewritten only after the next barrier
+      if (a.stages == 1) {
+        __syncthreads();
+        if (tid == 0) issue_next(0);
+      }
+      continue;
+    }
+    __syncthreads();
+
+    // 3. emit finished rows in probe order at the unit's offset
+    const uint32_t bsh4 = (uint32_t)(inf.b_lo & 3), bsh8 = (uint32_t)(inf.b_lo & 1);
+    const uint32_t qsh4 = (uint32_t)(inf.q_lo & 3), qsh8 = (uint32_t)(inf.q_lo & 1);
+    auto write_row = [&](uint64_t oo, uint32_t li, uint32_t jl, K k) {
+      const uint64_t gi = inf.b_lo + li, j = inf.q_lo + jl;
+      if (a.key_out) static_cast<K*>(a.key_out)[oo] = k;
+      if (a.ids_r) a.ids_r[oo] = a.carried_r ? a.carried_r[gi] : (uint32_t)gi;
+      if (a.ids_s) a.ids_s[oo] = a.carried_s ? a.carried_s[j] : (uint32_t)j;
+      for (int c = 0; c < a.nr; ++c) {
+        if (a.r_bytes[c] == 4)
+          static_cast<uint32_t*>(a.r_dst[c])[oo] = reinterpret_cast<const uint32_t*>(st + a.off_r[c])[bsh4 + li];
+        else
+          static_cast<uint64_t*>(a.r_dst[c])[oo] = reinterpret_cast<const uint64_t*>(st + a.off_r[c])[bsh8 + li];
+      }
+      for (int c = 0; c < a.ns; ++c) {
+        if (a.s_bytes[c] == 4)
+          static_cast<uint32_t*>(a.s_dst[c])[oo] = reinterpret_cast<const uint32_t*>(st + a.off_s[c])[qsh4 + jl];
+        else
+          static_cast<uint64_t*>(a.s_dst[c])[oo] = reinterpret_cast<const uint64_t*>(st + a.off_s[c])[qsh8 + jl];
+      }
+    };
+    uint64_t o = s_wbase[warp];
+    for (uint32_t r = r0; r < r1; ++r) {
+      const uint32_t jl = r * 32 + lane;
+      const uint32_t e = jl < nq ? res[jl] : kNoMatch;
+      if (!has_dup) {
+        const bool hit = e != kNoMatch;
+        const uint32_t bal = __ballot_sync(0xffffffffu, hit);
+        if (hit) {
+          const uint64_t oo = o + __popc(bal & dev::lanemask_lt());
+          if (oo < a.capacity) write_row(oo, e, jl, bk[e]);
+        }
+        o += __popc(bal);
+      } else {
+        const uint32_t m = e == kNoMatch ? 0 : (e & 0xffffu);
+        const uint32_t lb = e >> 16;
+        const uint32_t inc = dev::warp_inclusive_sum(m);
+        uint64_t oo = o + inc - m;
+        for (uint32_t t = 0; t < m; ++t, ++oo) {
+          const uint32_t li = sidx[lb + t];
+          if (oo < a.capacity) write_row(oo, li, jl, bk[li]);
+        }
+        o += __shfl_sync(0xffffffffu, inc, 31);
+      }
+    }
+    __syncthreads();
+    if (a.stages == 1 && tid == 0) issue_next(0);
+  }
+}
+
 struct Plan {
   uint64_t total_units = 0;
   uint64_t max_chunk = 0;
@@ -353,15 +656,49 @@ struct Plan {
 Plan make_plan(cj_ctx* ctx, const uint64_t* boff, const uint64_t* poff, uint32_t fanout,
                uint32_t limit, uint64_t* unit_start) {
   Scratch st(ctx, 2 * sizeof(uint64_t));
-  PlanArgs pa{boff, poff, fanout, limit, kProbeChunk, unit_start, st.as<uint64_t>()};
+  CJ_CUDA(cudaMemsetAsync(st.p, 0, 2 * sizeof(uint64_t), ctx->stream));
+  const uint32_t blocks = (fanout + kPlanThreads * kPlanPer - 1) / (kPlanThreads * kPlanPer);
+  PlanArgs2 pa{boff, poff, fanout, limit, probe_chunk(), unit_start,
+               st.as<unsigned long long>(), ctx->status_buffer(blocks), 0, ctx->err_word};
+  pa.epoch = ctx->next_epoch();
   ctx->kbegin("phj_plan", 16ull * fanout);
-  k_phj_plan<<<1, 1024, 0, ctx->stream>>>(pa);
+  k_phj_plan<<<blocks, kPlanThreads, 0, ctx->stream>>>(pa);
   ctx->kend();
   CJ_CUDA(cudaGetLastError());
   uint64_t* h = reinterpret_cast<uint64_t*>(ctx->host_pinned);
   CJ_CUDA(cudaMemcpyAsync(h, st.p, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
   CJ_CUDA(cudaStreamSynchronize(ctx->stream));
   return Plan{h[1], h[0]};
+}
+
+void atomicOr_host_overflow(cj_ctx* ctx) {
+  const uint32_t v = kErrOverflow;
+  CJ_CUDA(cudaMemcpyAsync(ctx->err_word, &v, 4, cudaMemcpyHostToDevice, ctx->stream));
+  CJ_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+template <class K>
+bool tma_layout(FindArgs& a, size_t* smem_out) {
+  auto up = [](size_t x) { return (x + 127) & ~size_t(127); };
+  const uint32_t kb = sizeof(K);
+  size_t off = 0;
+  a.off_bk = (uint32_t)off;
+  off = up(off + (size_t)(a.max_chunk + 8) * kb);
+  for (int c = 0; c < a.nr; ++c) {
+    a.off_r[c] = (uint32_t)off;
+    off = up(off + (size_t)(a.max_chunk + 8) * a.r_bytes[c]);
+  }
+  a.off_pk = (uint32_t)off;
+  off = up(off + (size_t)(a.qchunk + 8) * kb);
+  for (int c = 0; c < a.ns; ++c) {
+    a.off_s[c] = (uint32_t)off;
+    off = up(off + (size_t)(a.qchunk + 8) * a.s_bytes[c]);
+  }
+  a.stage_bytes = (uint32_t)off;
+  a.cap_entries = 1u << a.cap_log2;
+  const size_t smem = (size_t)a.stages * off + up(2 * (size_t)a.cap_entries) + (size_t)a.qchunk * 4;
+  *smem_out = smem;
+  return smem <= 210 * 1024;
 }
 
 template <class K>
@@ -376,40 +713,98 @@ uint64_t run_find(cj_ctx* ctx, FindArgs a, uint64_t total_units) {
   uint32_t cap_log2 = 1;
   while ((1ull << cap_log2) < 2ull * a.max_chunk) ++cap_log2;
   a.cap_log2 = cap_log2;
-  size_t stage = 0;
-  if (a.write && a.nr > 0) {
-    for (int c = 0; c < a.nr; ++c) {
-      a.r_stage_off[c] = (uint32_t)stage;
-      stage += (size_t)a.max_chunk * a.r_bytes[c];
-      stage = (stage + 15) & ~size_t(15);
+  size_t tma_smem = 0;
+  const char* mode = std::getenv("CJ_FIND");
+  const bool want_tma = !(mode && std::strcmp(mode, "ldg") == 0);
+  if (want_tma && a.padded && a.desc && tma_layout<K>(a, &tma_smem)) {
+    // count pass (keys only) -> scan -> fill pass; no inter-CTA waiting
+    const uint64_t U = total_units;
+    uint64_t total = 0;
+    if (U > 0) {
+      Scratch counts(ctx, U * 8), offs(ctx, U * 8);
+      FindArgs ac = a;
+      ac.nr = ac.ns = 0;
+      ac.unit_counts = counts.as<uint64_t>();
+      size_t smem_c = 0;
+      tma_layout<K>(ac, &smem_c);
+      const unsigned grid =
+          (unsigned)std::min<uint64_t>((uint64_t)ctx->num_sms * find_ctas_per_sm(), U);
+      CJ_CUDA(cudaFuncSetAttribute(k_phj_tma<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem_c));
+      ctx->kbegin("phj_count", (uint64_t)(sizeof(K)) * (a.nb_rows + a.np_rows));
+      k_phj_tma<K, false><<<grid, kTmaThreads, smem_c, ctx->stream>>>(ac);
+      ctx->kend();
+      scan_counts(ctx, counts.as<uint64_t>(), U, offs.as<uint64_t>(), a.total_out);
+      CJ_CUDA(cudaGetLastError());
+      uint64_t* h = reinterpret_cast<uint64_t*>(ctx->host_pinned);
+      CJ_CUDA(cudaMemcpyAsync(h, a.total_out, 8, cudaMemcpyDeviceToHost, ctx->stream));
+      CJ_CUDA(cudaStreamSynchronize(ctx->stream));
+      total = h[0];
+      if (a.write) {
+        if (total > a.capacity) {
+          CJ_CUDA(cudaMemsetAsync(a.err, 0, 4, ctx->stream));
+          atomicOr_host_overflow(ctx);
+        } else {
+          a.unit_off = offs.as<uint64_t>();
+          CJ_CUDA(cudaFuncSetAttribute(k_phj_tma<K, true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tma_smem));
+          ctx->kbegin("phj_find", 0);
+          k_phj_tma<K, true><<<grid, kTmaThreads, tma_smem, ctx->stream>>>(a);
+          ctx->kend();
+          CJ_CUDA(cudaGetLastError());
+          CJ_CUDA(cudaStreamSynchronize(ctx->stream));
+        }
+      }
     }
-  }
-  size_t smem = (size_t)a.max_chunk * sizeof(K);
-  smem = (smem + 15) & ~size_t(15);
-  smem += (size_t)2 << cap_log2;
-  smem += (size_t)a.qchunk * 4;
-  a.stage_r = 0;
-  if (stage && smem + stage <= 160 * 1024) {
-    a.stage_r = 1;
-    smem += stage;
-  }
-  if (smem > 200 * 1024) fail(CJ_ERR_CAPACITY_EXCEEDED, "hash join: build chunk exceeds shared memory");
-  CJ_CUDA(cudaFuncSetAttribute(k_phj_find<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem));
-  int per_sm = 0;
-  CJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_phj_find<K>, kThreads, smem));
-  per_sm = std::max(per_sm, 1);
-  const uint64_t grid = std::min<uint64_t>((uint64_t)ctx->num_sms * per_sm, total_units);
-  if (total_units > 0) {
-    ctx->kbegin(a.write ? "phj_find" : "phj_count", 0);
-    k_phj_find<K><<<(unsigned)grid, kThreads, smem, ctx->stream>>>(a);
-    ctx->kend();
-    CJ_CUDA(cudaGetLastError());
+    return total;
+  } else {
+    size_t stage = 0;
+    if (a.write && a.nr > 0) {
+      for (int c = 0; c < a.nr; ++c) {
+        a.r_stage_off[c] = (uint32_t)stage;
+        stage += (size_t)a.max_chunk * a.r_bytes[c];
+        stage = (stage + 15) & ~size_t(15);
+      }
+    }
+    size_t smem = (size_t)a.max_chunk * sizeof(K);
+    smem = (smem + 15) & ~size_t(15);
+    smem += (size_t)2 << cap_log2;
+    smem += (size_t)a.qchunk * 4;
+    a.stage_r = 0;
+    if (stage && smem + stage <= 160 * 1024) {
+      a.stage_r = 1;
+      smem += stage;
+    }
+    if (smem > 200 * 1024) fail(CJ_ERR_CAPACITY_EXCEEDED, "hash join: build chunk exceeds shared memory");
+    CJ_CUDA(cudaFuncSetAttribute(k_phj_find<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    int per_sm = 0;
+    CJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_phj_find<K>, kThreads, smem));
+    per_sm = std::max(per_sm, 1);
+    const uint64_t grid = std::min<uint64_t>((uint64_t)ctx->num_sms * per_sm, total_units);
+    if (total_units > 0) {
+      ctx->kbegin(a.write ? "phj_find" : "phj_count", 0);
+      k_phj_find<K><<<(unsigned)grid, kThreads, smem, ctx->stream>>>(a);
+      ctx->kend();
+      CJ_CUDA(cudaGetLastError());
+    }
   }
   uint64_t* h = reinterpret_cast<uint64_t*>(ctx->host_pinned);
   CJ_CUDA(cudaMemcpyAsync(h, tot.p, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
   CJ_CUDA(cudaStreamSynchronize(ctx->stream));
   return h[0];
+}
+
+// Precomputed unit descriptors for the TMA passes.
+void build_desc(cj_ctx* ctx, FindArgs& a, uint64_t total_units, Scratch& desc) {
+  if (total_units == 0) return;
+  ctx->kbegin("phj_desc", total_units * 32);
+  k_phj_desc<<<grid_for(a.fanout, 256, 1024), 256, 0, ctx->stream>>>(
+      a.boff, a.poff, a.unit_start, a.fanout, a.limit, a.qchunk, desc.as<UnitDesc>());
+  ctx->kend();
+  CJ_CUDA(cudaGetLastError());
+  a.desc = desc.p;
+  a.n_units = total_units;
 }
 
 FindArgs base_args(const void* bkeys, const uint64_t* boff, const void* pkeys,
@@ -421,7 +816,8 @@ FindArgs base_args(const void* bkeys, const uint64_t* boff, const void* pkeys,
   a.poff = poff;
   a.fanout = fanout;
   a.limit = limit;
-  a.qchunk = kProbeChunk;
+  a.qchunk = probe_chunk();
+  a.stages = find_stages();
   return a;
 }
 
@@ -444,6 +840,11 @@ uint64_t phj_find(cj_ctx* ctx, const void* bkeys, const uint64_t* boff, const vo
   a.max_chunk = (uint32_t)std::max<uint64_t>(plan.max_chunk, 1);
   a.write = 1;
   a.capacity = capacity;
+  a.padded = out.padded ? 1 : 0;
+  a.nb_rows = out.r_rows;
+  a.np_rows = out.s_rows;
+  Scratch desc(ctx, std::max<uint64_t>(plan.total_units, 1) * sizeof(UnitDesc));
+  if (a.padded) build_desc(ctx, a, plan.total_units, desc);
   a.key_out = out.key;
   a.ids_r = out.ids_r;
   a.ids_s = out.ids_s;

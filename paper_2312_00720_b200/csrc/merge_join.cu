@@ -20,6 +20,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 #include "cj_device.cuh"
 #include "cj_internal.cuh"
@@ -58,6 +60,12 @@ struct SmjArgs {
   void* s_dst[CJ_MAX_COLS];
   uint32_t r_bytes[CJ_MAX_COLS];
   uint32_t s_bytes[CJ_MAX_COLS];
+  // TMA count / fill passes
+  const void* desc;          // SmjDesc[tiles]
+  uint64_t* tile_counts;
+  uint64_t* tile_off;
+  uint32_t stage_bytes, off_rk, off_sk, off_r[CJ_MAX_COLS], off_s[CJ_MAX_COLS];
+  int padded;
 };
 
 template <class K>
@@ -208,6 +216,289 @@ __global__ void __launch_bounds__(kThreads) k_smj_find(const __grid_constant__ S
   }
 }
 
+// ---- TMA-pipelined count / fill (the default for run_join) ------------------
+//
+// Tiles of 2048 probe rows; a bounds kernel finds every tile's r window
+// [lower_bound(s[j0]), upper_bound(s[j1-1])) with one binary search per tile
+// (all tiles in parallel).  Count and fill passes are persistent (one CTA of
+// 512 threads per SM, tile t_k = blockIdx + k * gridDim), bulk-copy the window
+// (keys + transformed R payloads) and the probe tile (keys + transformed S
+// payloads) into one of two shared-memory stages while the previous tile is
+// merged, and chain nothing across CTAs: counts -> scan -> fill.
+constexpr int kTmaThreads = 512;
+constexpr int kTmaWarps = kTmaThreads / 32;
+
+struct SmjDesc {
+  uint64_t r_lo, r_hi, s_lo, s_hi;
+};
+
+template <class K>
+__global__ void k_smj_bounds(const K* __restrict__ r, uint64_t nr, const K* __restrict__ s,
+                             uint64_t ns, uint64_t tiles, SmjDesc* __restrict__ desc) {
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < tiles;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    SmjDesc d;
+    d.s_lo = t * kTileS;
+    d.s_hi = dev::umin64(ns, d.s_lo + kTileS);
+    d.r_lo = g_lower_bound<K>(r, 0, nr, s[d.s_lo]);
+    d.r_hi = g_upper_bound<K>(r, d.r_lo, nr, s[d.s_hi - 1]);
+    desc[t] = d;
+  }
+}
+
+template <class K, bool WRITE>
+__global__ void __launch_bounds__(kTmaThreads, 1) k_smj_tma(const __grid_constant__ SmjArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint32_t* loff = reinterpret_cast<uint32_t*>(smem + 2 * (size_t)a.stage_bytes);
+  uint32_t* mcnt = loff + kTileS;
+  __shared__ SmjDesc s_desc[2];
+  __shared__ __align__(8) uint64_t mbar[2];
+  __shared__ uint64_t s_wcount[kTmaWarps], s_wbase[kTmaWarps];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const SmjDesc* __restrict__ descs = static_cast<const SmjDesc*>(a.desc);
+  const K* __restrict__ rg = static_cast<const K*>(a.r);
+  const uint32_t kb = sizeof(K);
+  auto bytes = [&](uint64_t lo, uint64_t hi, uint32_t w) {
+    return hi > lo ? (uint32_t)((dev::align_hi(hi, w) - dev::align_lo(lo, w)) * w) : 0u;
+  };
+  auto issue = [&](int b, const SmjDesc& d) {  // thread 0
+    uint8_t* st = smem + (size_t)b * a.stage_bytes;
+    const bool win = d.r_hi - d.r_lo <= a.wmax;
+    uint32_t total = bytes(d.s_lo, d.s_hi, kb);
+    if (win) total += bytes(d.r_lo, d.r_hi, kb);
+    if (WRITE) {
+      if (win)
+        for (int c = 0; c < a.nr_cols; ++c) total += bytes(d.r_lo, d.r_hi, a.r_bytes[c]);
+      for (int c = 0; c < a.ns_cols; ++c) total += bytes(d.s_lo, d.s_hi, a.s_bytes[c]);
+    }
+    dev::mbar_expect_tx(&mbar[b], total);
+    auto copy = [&](uint32_t off, const void* base, uint64_t lo, uint64_t hi, uint32_t w) {
+      if (hi > lo)
+        dev::tma_load_1d(st + off, static_cast<const uint8_t*>(base) + dev::align_lo(lo, w) * w,
+                         bytes(lo, hi, w), &mbar[b]);
+    };
+    copy(a.off_sk, a.s, d.s_lo, d.s_hi, kb);
+    if (win) copy(a.off_rk, a.r, d.r_lo, d.r_hi, kb);
+    if (WRITE) {
+      if (win)
+        for (int c = 0; c < a.nr_cols; ++c) copy(a.off_r[c], a.r_src[c], d.r_lo, d.r_hi, a.r_bytes[c]);
+      for (int c = 0; c < a.ns_cols; ++c) copy(a.off_s[c], a.s_src[c], d.s_lo, d.s_hi, a.s_bytes[c]);
+    }
+  };
+  uint64_t t = blockIdx.x;
+  SmjDesc next{};
+  if (tid == 0) {
+    dev::mbar_init(&mbar[0], 1);
+    dev::mbar_init(&mbar[1], 1);
+    dev::fence_mbar_init();
+    if (t < a.tiles) {
+      s_desc[0] = descs[t];
+      issue(0, s_desc[0]);
+    }
+    if (t + gridDim.x < a.tiles) next = descs[t + gridDim.x];
+  }
+  __syncthreads();
+  uint32_t phase[2] = {0, 0};
+  int b = 0;
+  for (; t < a.tiles; t += gridDim.x, b ^= 1) {
+    const SmjDesc d = s_desc[b];
+    if (tid == 0 && t + gridDim.x < a.tiles) {
+      s_desc[b ^ 1] = next;
+      dev::fence_proxy_async();
+      issue(b ^ 1, next);
+      if (t + 2ull * gridDim.x < a.tiles) next = descs[t + 2ull * gridDim.x];
+    }
+    uint64_t tile_base = 0;
+    if (WRITE && tid == 32) tile_base = a.tile_off[t];
+    uint8_t* st = smem + (size_t)b * a.stage_bytes;
+    const uint32_t nq = (uint32_t)(d.s_hi - d.s_lo);
+    const uint64_t w = d.r_hi - d.r_lo;
+    const bool win = w <= a.wmax;
+    const K* sk = reinterpret_cast<const K*>(st + a.off_sk) + (d.s_lo - dev::align_lo(d.s_lo, kb));
+    const K* rk = reinterpret_cast<const K*>(st + a.off_rk) + (d.r_lo - dev::align_lo(d.r_lo, kb));
+    dev::mbar_wait(&mbar[b], phase[b]);
+    phase[b] ^= 1;
+    __syncthreads();
+
+    const uint32_t rounds = (nq + 31) / 32;
+    const uint32_t r0 = rounds * warp / kTmaWarps, r1 = rounds * (warp + 1) / kTmaWarps;
+    uint64_t wc = 0;
+    for (uint32_t rr = r0; rr < r1; ++rr) {
+      const uint32_t jl = rr * 32 + lane;
+      if (jl >= nq) continue;
+      const K k = sk[jl];
+      uint64_t lb, m = 0;
+      if (win) {
+        uint32_t lo = 0, hi = (uint32_t)w;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (rk[mid] < k) lo = mid + 1; else hi = mid;
+        }
+        lb = lo;
+        if (lo < w && rk[lo] == k) {
+          if (a.pk_fk) {
+            m = 1;
+          } else {
+            uint32_t lo2 = lo + 1, hi2 = (uint32_t)w;
+            while (lo2 < hi2) {
+              const uint32_t mid = (lo2 + hi2) >> 1;
+              if (rk[mid] <= k) lo2 = mid + 1; else hi2 = mid;
+            }
+            m = lo2 - lo;
+          }
+        }
+      } else {
+        const uint64_t g = g_lower_bound<K>(rg, d.r_lo, d.r_hi, k);
+        lb = g - d.r_lo;
+        if (g < d.r_hi && rg[g] == k) m = a.pk_fk ? 1 : g_upper_bound<K>(rg, g, d.r_hi, k) - g;
+      }
+      if (WRITE) {
+        loff[jl] = (uint32_t)lb;
+        mcnt[jl] = (uint32_t)m;
+      }
+      wc += m;
+    }
+    wc = dev::warp_sum(wc);
+    if (lane == 0) s_wcount[warp] = wc;
+    __syncthreads();
+    if (warp == 1) {
+      const uint64_t v = lane < kTmaWarps ? s_wcount[lane] : 0;
+      const uint64_t inc = dev::warp_inclusive_sum(v);
+      const uint64_t base = __shfl_sync(0xffffffffu, tile_base, 0);
+      if (lane < kTmaWarps) s_wbase[lane] = base + inc - v;
+      if (!WRITE && lane == kTmaWarps - 1) a.tile_counts[t] = inc;
+    }
+    if (!WRITE) continue;
+    __syncthreads();
+    const uint32_t ssh4 = (uint32_t)(d.s_lo & 3), ssh8 = (uint32_t)(d.s_lo & 1);
+    const uint32_t rsh4 = (uint32_t)(d.r_lo & 3), rsh8 = (uint32_t)(d.r_lo & 1);
+    uint64_t o = s_wbase[warp];
+    for (uint32_t rr = r0; rr < r1; ++rr) {
+      const uint32_t jl = rr * 32 + lane;
+      const uint32_t m = jl < nq ? mcnt[jl] : 0;
+      const uint32_t inc = dev::warp_inclusive_sum(m);
+      uint64_t oo = o + inc - m;
+      if (m) {
+        const uint64_t j = d.s_lo + jl;
+        const K k = sk[jl];
+        const uint32_t l0 = loff[jl];
+        for (uint32_t q = 0; q < m; ++q, ++oo) {
+          if (oo >= a.capacity) continue;
+          const uint32_t li = l0 + q;
+          const uint64_t i = d.r_lo + li;
+          if (a.key_out) static_cast<K*>(a.key_out)[oo] = k;
+          if (a.ids_r) a.ids_r[oo] = a.carried_r ? a.carried_r[i] : (uint32_t)i;
+          if (a.ids_s) a.ids_s[oo] = a.carried_s ? a.carried_s[j] : (uint32_t)j;
+          for (int c = 0; c < a.nr_cols; ++c) {
+            if (a.r_bytes[c] == 4)
+              static_cast<uint32_t*>(a.r_dst[c])[oo] =
+                  win ? reinterpret_cast<const uint32_t*>(st + a.off_r[c])[rsh4 + li]
+                      : static_cast<const uint32_t*>(a.r_src[c])[i];
+            else
+              static_cast<uint64_t*>(a.r_dst[c])[oo] =
+                  win ? reinterpret_cast<const uint64_t*>(st + a.off_r[c])[rsh8 + li]
+                      : static_cast<const uint64_t*>(a.r_src[c])[i];
+          }
+          for (int c = 0; c < a.ns_cols; ++c) {
+            if (a.s_bytes[c] == 4)
+              static_cast<uint32_t*>(a.s_dst[c])[oo] =
+                  reinterpret_cast<const uint32_t*>(st + a.off_s[c])[ssh4 + jl];
+            else
+              static_cast<uint64_t*>(a.s_dst[c])[oo] =
+                  reinterpret_cast<const uint64_t*>(st + a.off_s[c])[ssh8 + jl];
+          }
+        }
+      }
+      o += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    __syncthreads();
+  }
+}
+
+template <class K>
+size_t smj_layout_w(SmjArgs& a, bool write, uint32_t wmax) {
+  auto up = [](size_t x) { return (x + 127) & ~size_t(127); };
+  const uint32_t kb = sizeof(K);
+  const uint32_t kWinMax = wmax;
+  a.wmax = wmax;
+  size_t off = 0;
+  a.off_rk = (uint32_t)off;
+  off = up(off + (size_t)(kWinMax + 8) * kb);
+  if (write)
+    for (int c = 0; c < a.nr_cols; ++c) {
+      a.off_r[c] = (uint32_t)off;
+      off = up(off + (size_t)(kWinMax + 8) * a.r_bytes[c]);
+    }
+  a.off_sk = (uint32_t)off;
+  off = up(off + (size_t)(kTileS + 8) * kb);
+  if (write)
+    for (int c = 0; c < a.ns_cols; ++c) {
+      a.off_s[c] = (uint32_t)off;
+      off = up(off + (size_t)(kTileS + 8) * a.s_bytes[c]);
+    }
+  a.stage_bytes = (uint32_t)off;
+  return 2 * off + 2 * sizeof(uint32_t) * kTileS;
+}
+
+// Largest r window (shared-memory keys + R payloads) whose two stages fit.
+template <class K>
+size_t smj_layout(SmjArgs& a, bool write) {
+  size_t smem = 0;
+  for (uint32_t w : {4096u, 2048u, 1024u, 512u}) {
+    smem = smj_layout_w<K>(a, write, w);
+    if (smem <= 200 * 1024) break;
+  }
+  return smem;
+}
+
+template <class K>
+uint64_t run_tma(cj_ctx* ctx, SmjArgs a) {
+  a.tiles = (a.ns + kTileS - 1) / kTileS;
+  Scratch tot(ctx, 8);
+  CJ_CUDA(cudaMemsetAsync(tot.p, 0, 8, ctx->stream));
+  if (a.tiles == 0 || a.nr == 0) return 0;
+  Scratch desc(ctx, a.tiles * sizeof(SmjDesc)), counts(ctx, a.tiles * 8), offs(ctx, a.tiles * 8);
+  a.desc = desc.p;
+  ctx->kbegin("smj_bounds", a.tiles * (2 * sizeof(K) + 32));
+  k_smj_bounds<K><<<grid_for(a.tiles, 128, 4096), 128, 0, ctx->stream>>>(
+      static_cast<const K*>(a.r), a.nr, static_cast<const K*>(a.s), a.ns, a.tiles,
+      desc.as<SmjDesc>());
+  ctx->kend();
+  SmjArgs ac = a;
+  ac.tile_counts = counts.as<uint64_t>();
+  const size_t smem_c = smj_layout<K>(ac, false);
+  const unsigned grid = (unsigned)std::min<uint64_t>((uint64_t)ctx->num_sms, a.tiles);
+  CJ_CUDA(cudaFuncSetAttribute(k_smj_tma<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem_c));
+  ctx->kbegin("smj_count", sizeof(K) * (a.nr + a.ns));
+  k_smj_tma<K, false><<<grid, kTmaThreads, smem_c, ctx->stream>>>(ac);
+  ctx->kend();
+  scan_counts(ctx, counts.as<uint64_t>(), a.tiles, offs.as<uint64_t>(), tot.as<uint64_t>());
+  CJ_CUDA(cudaGetLastError());
+  uint64_t* h = reinterpret_cast<uint64_t*>(ctx->host_pinned);
+  CJ_CUDA(cudaMemcpyAsync(h, tot.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CJ_CUDA(cudaStreamSynchronize(ctx->stream));
+  const uint64_t total = h[0];
+  if (!a.write) return total;
+  if (total > a.capacity) {
+    const uint32_t v = kErrOverflow;
+    CJ_CUDA(cudaMemcpyAsync(ctx->err_word, &v, 4, cudaMemcpyHostToDevice, ctx->stream));
+    CJ_CUDA(cudaStreamSynchronize(ctx->stream));
+    return total;
+  }
+  a.tile_off = offs.as<uint64_t>();
+  const size_t smem = smj_layout<K>(a, true);
+  if (smem > 220 * 1024) fail(CJ_ERR_UNSUPPORTED, "merge join stage exceeds shared memory");
+  CJ_CUDA(cudaFuncSetAttribute(k_smj_tma<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem));
+  ctx->kbegin("smj_find", 0);
+  k_smj_tma<K, true><<<grid, kTmaThreads, smem, ctx->stream>>>(a);
+  ctx->kend();
+  CJ_CUDA(cudaGetLastError());
+  CJ_CUDA(cudaStreamSynchronize(ctx->stream));
+  return total;
+}
+
 template <class K>
 __global__ void k_check_sorted(const K* __restrict__ v, uint64_t n, int strict,
                                uint32_t* err, uint32_t code) {
@@ -285,7 +576,12 @@ uint64_t smj_find(cj_ctx* ctx, const void* rkeys, uint64_t nr, const void* skeys
     a.s_dst[c] = out.s_dst[c];
     a.s_bytes[c] = out.s_bytes[c];
   }
-  const uint64_t t = key_bytes == 4 ? run<uint32_t>(ctx, a) : run<uint64_t>(ctx, a);
+  a.padded = out.padded ? 1 : 0;
+  const char* mode = std::getenv("CJ_FIND");
+  const bool tma = a.padded && !(mode && std::strcmp(mode, "ldg") == 0);
+  uint64_t t;
+  if (tma) t = key_bytes == 4 ? run_tma<uint32_t>(ctx, a) : run_tma<uint64_t>(ctx, a);
+  else t = key_bytes == 4 ? run<uint32_t>(ctx, a) : run<uint64_t>(ctx, a);
   raise_device_errors(ctx);
   return t;
 }

@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "cj_device.cuh"
@@ -31,53 +32,86 @@ using dev::kFlagIncl;
 using dev::kValMask;
 
 constexpr int kHistThreads = 512;
+constexpr int kHistWarps = kHistThreads / 32;
+constexpr int kHistSub = 4;  // CTAs per static block in the counting kernel
 
+// Per-block digit counts of every pass in one read of the keys.  Block b owns
+// the contiguous tile range [b*tiles/nblocks, (b+1)*tiles/nblocks) — the same
+// static ranges the scatter kernel walks — so the counts double as the
+// scatter's cross-block cursors (no look-back).  cnt[b][p][d].
 template <class K>
 __global__ void __launch_bounds__(kHistThreads)
-k_histogram(const K* __restrict__ keys, uint64_t n, int npasses, uint4 shifts_lo, uint4 shifts_hi,
-            uint4 masks_lo, uint4 masks_hi, uint32_t* __restrict__ counts) {
-  extern __shared__ uint32_t sh[];  // npasses * 256
+k_block_hist(const K* __restrict__ keys, uint64_t n, uint64_t tile, uint64_t tiles,
+             uint32_t nblocks, int npasses, uint4 shifts_lo, uint4 shifts_hi, uint4 masks_lo,
+             uint4 masks_hi, uint32_t hparts, uint32_t* __restrict__ cnt) {
+  extern __shared__ uint32_t sh[];  // [warp][npasses * 256]
   const uint32_t sh_arr[8] = {shifts_lo.x, shifts_lo.y, shifts_lo.z, shifts_lo.w,
                               shifts_hi.x, shifts_hi.y, shifts_hi.z, shifts_hi.w};
   const uint32_t mk_arr[8] = {masks_lo.x, masks_lo.y, masks_lo.z, masks_lo.w,
                               masks_hi.x, masks_hi.y, masks_hi.z, masks_hi.w};
-  for (int i = threadIdx.x; i < npasses * kRadix; i += blockDim.x) sh[i] = 0;
+  const int width = npasses * kRadix;
+  for (int i = threadIdx.x; i < kHistWarps * width; i += kHistThreads) sh[i] = 0;
   __syncthreads();
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint32_t* mine = sh + (threadIdx.x >> 5) * width;
+  // gridDim.x = nblocks * kHistSub: sub-CTA s of block b counts a quarter of
+  // the block's tiles and adds into cnt[b] (zeroed by the caller)
+  const uint64_t b = blockIdx.x / kHistSub, sub = blockIdx.x % kHistSub;
+  const uint64_t t0 = b * tiles / nblocks, t1 = (b + 1) * tiles / nblocks;
+  const uint64_t lo = dev::umin64(n, (t0 + sub * (t1 - t0) / kHistSub) * tile);
+  const uint64_t hi = dev::umin64(n, (t0 + (sub + 1) * (t1 - t0) / kHistSub) * tile);
   auto count = [&](K k) {
 #pragma unroll
     for (int p = 0; p < 8; ++p)
-      if (p < npasses) atomicAdd(&sh[p * kRadix + (uint32_t)((k >> sh_arr[p]) & mk_arr[p])], 1u);
+      if (p < npasses)
+        atomicAdd(&mine[p * kRadix + dev::key_digit(k, sh_arr[p], mk_arr[p], hparts)], 1u);
   };
   constexpr int kVec = 16 / sizeof(K);
-  const bool aligned = (reinterpret_cast<uintptr_t>(keys) & 15u) == 0;
-  uint64_t start = 0;
-  if (aligned) {
-    const uint64_t nvec = n / kVec;
-    const uint4* kv = reinterpret_cast<const uint4*>(keys);
-    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += stride) {
+  uint64_t i = lo;
+  if ((reinterpret_cast<uintptr_t>(keys + lo) & 15u) == 0) {
+    const uint4* kv = reinterpret_cast<const uint4*>(keys + lo);
+    const uint64_t nvec = (hi - lo) / kVec;
+    uint64_t v = threadIdx.x;
+    for (; v + 3 * kHistThreads < nvec; v += 4 * kHistThreads) {  // 4 loads in flight
+      uint4 q[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) q[u] = __ldcs(kv + v + u * kHistThreads);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        K e[kVec];
+        memcpy(e, &q[u], 16);
+#pragma unroll
+        for (int j = 0; j < kVec; ++j) count(e[j]);
+      }
+    }
+    for (; v < nvec; v += kHistThreads) {
       uint4 q = __ldcs(kv + v);
       K e[kVec];
       memcpy(e, &q, 16);
 #pragma unroll
       for (int j = 0; j < kVec; ++j) count(e[j]);
     }
-    start = nvec * kVec;
+    i = lo + nvec * kVec;
   }
-  for (uint64_t i = start + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-    count(keys[i]);
+  for (uint64_t j = i + threadIdx.x; j < hi; j += kHistThreads) count(keys[j]);
   __syncthreads();
-  for (int i = threadIdx.x; i < npasses * kRadix; i += blockDim.x)
-    if (sh[i]) atomicAdd(&counts[i], sh[i]);
+  for (int d = threadIdx.x; d < width; d += kHistThreads) {
+    uint32_t t = 0;
+#pragma unroll
+    for (int w = 0; w < kHistWarps; ++w) t += sh[w * width + d];
+    if (t) atomicAdd(&cnt[b * width + d], t);
+  }
 }
 
-// Exclusive digit bases per pass (digit order), 1 block of 256 threads.
-__global__ void k_digit_bases(const uint32_t* __restrict__ counts, int npasses,
-                              uint64_t* __restrict__ base) {
+// Totals and exclusive digit bases per pass from the per-block counts
+// (1 block of 256 threads; thread d owns digit d).
+__global__ void k_digit_bases(const uint32_t* __restrict__ cnt, uint32_t nblocks, int npasses,
+                              uint32_t* __restrict__ totals, uint64_t* __restrict__ base) {
   __shared__ uint64_t warp_tot[kRadix / 32];
   const int d = threadIdx.x;
   for (int p = 0; p < npasses; ++p) {
-    const uint64_t c = counts[p * kRadix + d];
+    uint64_t c = 0;
+    for (uint32_t b = 0; b < nblocks; ++b) c += cnt[((uint64_t)b * npasses + p) * kRadix + d];
+    totals[p * kRadix + d] = (uint32_t)c;
     const uint64_t inc = dev::warp_inclusive_sum(c);
     if ((d & 31) == 31) warp_tot[d >> 5] = inc;
     __syncthreads();
@@ -278,6 +312,247 @@ k_scatter_pass(const __grid_constant__ PassArgs a) {
   }
 }
 
+// ---- blocked scatter pass, TMA-pipelined (the default path) ---------------
+//
+// Persistent CTAs of 512 threads, one per SM; CTA b walks its static range of
+// consecutive tiles in order and carries the per-digit write cursors in shared
+// memory, so no CTA ever waits for another (the cross-block starting cursors
+// come from the per-block counts of k_block_hist).  While a tile is ranked and
+// written, the next tile's keys and carried columns stream into the other
+// shared-memory stage by cp.async.bulk.  Ranking uses bit ballots; lanes, item
+// rounds and warps are visited in input order, so the pass is stable.
+
+constexpr int kTmaThreads = 512;
+constexpr int kTmaWarps = kTmaThreads / 32;
+
+struct BlockPassArgs {
+  const void* keys_in;
+  void* keys_out;
+  uint64_t n, tiles;
+  uint32_t nblocks;
+  uint32_t shift, mask, bits;
+  uint32_t hparts;          // > 0: digit = shard of the key (key_digit)
+  const uint64_t* base;     // [256] exclusive digit base of this pass
+  const uint32_t* cnt;      // per-block counts of this pass: cnt[b * cnt_stride + d]
+  uint32_t cnt_stride;
+  uint32_t stage_bytes, pbytes;
+  int nvals, gen_ids;
+  int stages;               // 2: prefetch the next tile while this one runs
+  const void* vin[CJ_MAX_COLS + 1];
+  void* vout[CJ_MAX_COLS + 1];
+  uint32_t vbytes[CJ_MAX_COLS + 1];
+  uint32_t voff[CJ_MAX_COLS + 1];
+};
+
+template <class K, int ITEMS>
+__global__ void __launch_bounds__(kTmaThreads, 2)
+k_scatter_blocks(const __grid_constant__ BlockPassArgs a) {
+  constexpr uint32_t kTile = ITEMS * kTmaThreads;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* const stage0 = smem;
+  uint8_t* const P = smem + (size_t)a.stages * a.stage_bytes;
+  uint8_t* const sdig = P + a.pbytes;
+  __shared__ uint16_t whist[kTmaWarps][kRadix];
+  __shared__ uint32_t dstart[kRadix];
+  __shared__ uint64_t run[kRadix];   // next global position of each digit in this block
+  __shared__ uint64_t goff[kRadix];
+  __shared__ uint32_t wsum[kRadix / 32];
+  __shared__ __align__(8) uint64_t mbar[2];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const K* __restrict__ kin = static_cast<const K*>(a.keys_in);
+  const uint64_t blk = blockIdx.x;
+  const uint64_t t_begin = blk * a.tiles / a.nblocks, t_end = (blk + 1) * a.tiles / a.nblocks;
+
+  auto issue = [&](int b, uint64_t t) {  // thread 0: bulk-copy tile t into stage b
+    const uint64_t tb = t * kTile;
+    uint8_t* st = stage0 + (size_t)b * a.stage_bytes;
+    uint32_t total = kTile * sizeof(K);
+    for (int c = 0; c < a.nvals; ++c)
+      if (!(a.gen_ids && c == 0)) total += kTile * a.vbytes[c];
+    dev::mbar_expect_tx(&mbar[b], total);
+    dev::tma_load_1d(st, kin + tb, kTile * sizeof(K), &mbar[b]);
+    for (int c = 0; c < a.nvals; ++c)
+      if (!(a.gen_ids && c == 0))
+        dev::tma_load_1d(st + a.voff[c], static_cast<const uint8_t*>(a.vin[c]) + tb * a.vbytes[c],
+                         kTile * a.vbytes[c], &mbar[b]);
+  };
+  auto full_tile = [&](uint64_t t) { return (t + 1) * kTile <= a.n; };
+
+  if (tid == 0) {
+    dev::mbar_init(&mbar[0], 1);
+    dev::mbar_init(&mbar[1], 1);
+    dev::fence_mbar_init();
+    if (t_begin < t_end && full_tile(t_begin)) issue(0, t_begin);
+  }
+  // starting cursor of every digit: global base + counts of earlier blocks
+  if (tid < kRadix) {
+    uint64_t c = a.base[tid];
+    for (uint64_t b2 = 0; b2 < blk; ++b2) c += a.cnt[b2 * a.cnt_stride + tid];
+    run[tid] = c;
+  }
+  __syncthreads();
+
+  uint32_t phase[2] = {0, 0};
+  int b = 0;
+  for (uint64_t t = t_begin; t < t_end; ++t, b = (b + 1) % a.stages) {
+    if (a.stages == 2 && tid == 0 && t + 1 < t_end && full_tile(t + 1)) {
+      dev::fence_proxy_async();
+      issue(b ^ 1, t + 1);
+    }
+    for (int i = tid; i < kTmaWarps * kRadix; i += kTmaThreads) (&whist[0][0])[i] = 0;
+    const uint64_t tbase = t * kTile;
+    const uint32_t tile_n = (uint32_t)dev::umin64(kTile, a.n - tbase);
+    uint8_t* st = stage0 + (size_t)b * a.stage_bytes;
+    const K* skey = reinterpret_cast<const K*>(st);
+    if (full_tile(t)) {
+      dev::mbar_wait(&mbar[b], phase[b]);
+      phase[b] ^= 1;
+    } else {  // last, partial tile: plain loads
+      K* wk = reinterpret_cast<K*>(st);
+      for (uint32_t j = tid; j < kTile; j += kTmaThreads) wk[j] = j < tile_n ? kin[tbase + j] : K(0);
+      for (int c = 0; c < a.nvals; ++c) {
+        if (a.gen_ids && c == 0) continue;
+        if (a.vbytes[c] == 4) {
+          const uint32_t* src = static_cast<const uint32_t*>(a.vin[c]) + tbase;
+          uint32_t* dst = reinterpret_cast<uint32_t*>(st + a.voff[c]);
+          for (uint32_t j = tid; j < tile_n; j += kTmaThreads) dst[j] = src[j];
+        } else {
+          const uint64_t* src = static_cast<const uint64_t*>(a.vin[c]) + tbase;
+          uint64_t* dst = reinterpret_cast<uint64_t*>(st + a.voff[c]);
+          for (uint32_t j = tid; j < tile_n; j += kTmaThreads) dst[j] = src[j];
+        }
+      }
+    }
+    __syncthreads();
+
+    // 1. stable warp ranking over the warp's contiguous segment
+    const uint32_t wseg = warp * 32 * ITEMS;
+    K key[ITEMS];
+    uint32_t dig[ITEMS], rank[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const uint32_t li = wseg + i * 32 + lane;
+      const bool valid = li < tile_n;
+      const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
+      key[i] = skey[li];
+      const uint32_t d = valid ? dev::key_digit(key[i], a.shift, a.mask, a.hparts) : 0u;
+      const uint32_t peers = dev::digit_peers(d, a.bits, vmask);
+      const int leader = peers ? __ffs(peers) - 1 : lane;
+      uint32_t old = 0;
+      if (valid && lane == leader) {
+        old = whist[warp][d];
+        whist[warp][d] = (uint16_t)(old + __popc(peers));
+      }
+      old = __shfl_sync(0xffffffffu, old, leader);
+      rank[i] = old + __popc(peers & dev::lanemask_lt());
+      dig[i] = valid ? d : (uint32_t)kRadix;
+      __syncwarp();
+    }
+    __syncthreads();
+
+    // 2. per digit: exclusive prefix over warps and tile total; digit starts
+    uint32_t tile_count = 0, inc = 0;
+    if (tid < kRadix) {
+      uint32_t r = 0;
+#pragma unroll
+      for (int w = 0; w < kTmaWarps; ++w) {
+        const uint32_t c = whist[w][tid];
+        whist[w][tid] = (uint16_t)r;
+        r += c;
+      }
+      tile_count = r;
+      inc = dev::warp_inclusive_sum(tile_count);
+      if (lane == 31) wsum[warp] = inc;
+    }
+    __syncthreads();
+    if (tid < kRadix) {
+      uint32_t off = 0;
+#pragma unroll
+      for (int w = 0; w < kRadix / 32; ++w) off += w < warp ? wsum[w] : 0;
+      const uint32_t ds = off + inc - tile_count;
+      dstart[tid] = ds;
+      goff[tid] = run[tid] - ds;
+      run[tid] += tile_count;
+    }
+    __syncthreads();
+
+    // 3. keys to their tile-local sorted slots
+    uint32_t lpos[ITEMS];
+    K* pk = reinterpret_cast<K*>(P);
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      if (dig[i] < kRadix) {
+        lpos[i] = dstart[dig[i]] + whist[warp][dig[i]] + rank[i];
+        pk[lpos[i]] = key[i];
+        sdig[lpos[i]] = (uint8_t)dig[i];
+      } else {
+        lpos[i] = 0xffffffffu;
+      }
+    }
+    __syncthreads();
+
+    // 4. write keys digit-run by digit-run; remember each slot's destination
+    uint64_t gpos[ITEMS];
+    K* __restrict__ kout = static_cast<K*>(a.keys_out);
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+      const uint32_t j = tid + k * kTmaThreads;
+      if (j < tile_n) {
+        gpos[k] = goff[sdig[j]] + j;
+        kout[gpos[k]] = pk[j];
+      }
+    }
+
+    // 5. every carried column through the same permutation
+    for (int c = 0; c < a.nvals; ++c) {
+      const bool gen = a.gen_ids && c == 0;
+      __syncthreads();
+      if (a.vbytes[c] == 4) {
+        uint32_t* pv = reinterpret_cast<uint32_t*>(P);
+        const uint32_t* sv = reinterpret_cast<const uint32_t*>(st + a.voff[c]);
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i)
+          if (lpos[i] != 0xffffffffu)
+            pv[lpos[i]] = gen ? (uint32_t)(tbase + wseg + i * 32 + lane) : sv[wseg + i * 32 + lane];
+        __syncthreads();
+        uint32_t* __restrict__ vout = static_cast<uint32_t*>(a.vout[c]);
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) {
+          const uint32_t j = tid + k * kTmaThreads;
+          if (j < tile_n) vout[gpos[k]] = pv[j];
+        }
+      } else {
+        uint64_t* pv = reinterpret_cast<uint64_t*>(P);
+        const uint64_t* sv = reinterpret_cast<const uint64_t*>(st + a.voff[c]);
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i)
+          if (lpos[i] != 0xffffffffu)
+            pv[lpos[i]] = gen ? (uint64_t)(tbase + wseg + i * 32 + lane) : sv[wseg + i * 32 + lane];
+        __syncthreads();
+        uint64_t* __restrict__ vout = static_cast<uint64_t*>(a.vout[c]);
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) {
+          const uint32_t j = tid + k * kTmaThreads;
+          if (j < tile_n) vout[gpos[k]] = pv[j];
+        }
+      }
+    }
+    __syncthreads();
+    if (a.stages == 1 && tid == 0 && t + 1 < t_end && full_tile(t + 1)) {
+      dev::fence_proxy_async();
+      issue(0, t + 1);
+    }
+  }
+}
+
+template <class K, int ITEMS>
+void launch_blocks(cj_ctx* ctx, const BlockPassArgs& a, size_t smem) {
+  auto kern = k_scatter_blocks<K, ITEMS>;
+  CJ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<a.nblocks, kTmaThreads, smem, ctx->stream>>>(a);
+}
+
 // offsets[p] = first index whose low-`bits` digit is >= p (keys sorted by it)
 template <class K>
 __global__ void k_offsets(const K* __restrict__ keys, uint64_t n, uint32_t bits,
@@ -304,46 +579,155 @@ __global__ void k_iota(T* out, uint64_t n) {
 
 }  // namespace
 
-void histogram_passes(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes,
-                      const PassPlan& plan, uint32_t* counts_dev, uint64_t* base_dev,
-                      std::vector<uint32_t>* counts_host) {
+namespace {
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace
+
+ScatterGeom scatter_geom(cj_ctx* ctx, uint64_t n, int key_bytes, const ValCols& vals,
+                         const void* keys_in) {
+  ScatterGeom g;
+  uint64_t row = key_bytes;
+  uint32_t maxw = key_bytes;
+  bool al = aligned16(keys_in);
+  for (int c = 0; c < vals.n; ++c) {
+    const bool gen = vals.gen_ids && c == 0;
+    if (!gen) {
+      row += vals.bytes[c];
+      al = al && aligned16(vals.in[c]);
+    }
+    maxw = std::max(maxw, vals.bytes[c]);
+  }
+  const char* mode = std::getenv("CJ_SCATTER");
+  g.tma = al && !(mode && std::strcmp(mode, "ldg") == 0);
+  // tuning knobs (defaults chosen from the sweeps recorded in profiles/)
+  const char* e_items = std::getenv("CJ_SCATTER_ITEMS");
+  const char* e_ctas = std::getenv("CJ_SCATTER_CTAS");
+  const char* e_stages = std::getenv("CJ_SCATTER_STAGES");
+  const int want_items = e_items ? std::atoi(e_items) : 4;
+  g.ctas_per_sm = e_ctas ? std::max(1, std::atoi(e_ctas)) : 2;
+  g.stages = e_stages ? std::min(2, std::max(1, std::atoi(e_stages))) : 2;
+  const size_t budget = (g.ctas_per_sm >= 2 ? 100 : 200) * 1024;
+  for (int items : {8, 4, 2}) {
+    if (items > want_items && items > 2) continue;
+    g.items = items;
+    g.tile = (uint64_t)kTmaThreads * items;
+    g.stage_bytes = (uint32_t)(g.tile * row);
+    g.pbytes = (uint32_t)(g.tile * maxw);
+    g.smem = (size_t)g.stages * g.stage_bytes + g.pbytes + g.tile;
+    if (g.smem <= budget) break;
+  }
+  uint32_t off = (uint32_t)(g.tile * key_bytes);
+  for (int c = 0; c < vals.n; ++c) {
+    g.voff[c] = off;
+    if (!(vals.gen_ids && c == 0)) off += (uint32_t)(g.tile * vals.bytes[c]);
+  }
+  g.tiles = std::max<uint64_t>((n + g.tile - 1) / g.tile, 1);
+  g.nblocks = (uint32_t)std::min<uint64_t>(g.tiles, (uint64_t)ctx->num_sms * g.ctas_per_sm);
+  return g;
+}
+
+void block_hist(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes, const PassPlan& plan,
+                const ScatterGeom& g, uint32_t* cnt_dev, uint32_t hparts) {
   const int np = plan.npasses;
-  CJ_CUDA(cudaMemsetAsync(counts_dev, 0, sizeof(uint32_t) * kRadix * np, ctx->stream));
   uint32_t sh[8] = {}, mk[8] = {};
-  for (int p = 0; p < np; ++p) {
+  for (int p = 0; p < np && p < 8; ++p) {
     sh[p] = plan.lo[p];
     mk[p] = (1u << (plan.hi[p] - plan.lo[p])) - 1u;
   }
   const uint4 s_lo{sh[0], sh[1], sh[2], sh[3]}, s_hi{sh[4], sh[5], sh[6], sh[7]};
   const uint4 m_lo{mk[0], mk[1], mk[2], mk[3]}, m_hi{mk[4], mk[5], mk[6], mk[7]};
-  if (n > 0) {
-    const unsigned grid = grid_for(n, kHistThreads * 16, ctx->num_sms * 4);
-    const size_t smem = sizeof(uint32_t) * kRadix * np;
-    ctx->kbegin("histogram", n * key_bytes);
-    if (key_bytes == 4)
-      k_histogram<uint32_t><<<grid, kHistThreads, smem, ctx->stream>>>(
-          static_cast<const uint32_t*>(keys), n, np, s_lo, s_hi, m_lo, m_hi, counts_dev);
-    else
-      k_histogram<uint64_t><<<grid, kHistThreads, smem, ctx->stream>>>(
-          static_cast<const uint64_t*>(keys), n, np, s_lo, s_hi, m_lo, m_hi, counts_dev);
-    ctx->kend();
+  const size_t smem = sizeof(uint32_t) * kRadix * np * kHistWarps;
+  CJ_CUDA(cudaMemsetAsync(cnt_dev, 0, sizeof(uint32_t) * kRadix * np * g.nblocks, ctx->stream));
+  ctx->kbegin("histogram", n * key_bytes);
+  if (key_bytes == 4) {
+    CJ_CUDA(cudaFuncSetAttribute(k_block_hist<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    k_block_hist<uint32_t><<<g.nblocks * kHistSub, kHistThreads, smem, ctx->stream>>>(
+        static_cast<const uint32_t*>(keys), n, g.tile, g.tiles, g.nblocks, np, s_lo, s_hi, m_lo,
+        m_hi, hparts, cnt_dev);
+  } else {
+    CJ_CUDA(cudaFuncSetAttribute(k_block_hist<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    k_block_hist<uint64_t><<<g.nblocks * kHistSub, kHistThreads, smem, ctx->stream>>>(
+        static_cast<const uint64_t*>(keys), n, g.tile, g.tiles, g.nblocks, np, s_lo, s_hi, m_lo,
+        m_hi, hparts, cnt_dev);
   }
-  ctx->kbegin("digit_bases", 12ull * kRadix * np);
-  k_digit_bases<<<1, kRadix, 0, ctx->stream>>>(counts_dev, np, base_dev);
   ctx->kend();
   CJ_CUDA(cudaGetLastError());
-  if (counts_host) {
-    counts_host->resize((size_t)kRadix * np);
-    CJ_CUDA(cudaMemcpyAsync(ctx->host_pinned, counts_dev, sizeof(uint32_t) * kRadix * np,
+}
+
+void histogram_passes(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes,
+                      const PassPlan& plan, const ScatterGeom& g, uint32_t* cnt_dev,
+                      uint32_t* totals_dev, uint64_t* base_dev,
+                      std::vector<uint32_t>* totals_host, uint32_t hparts) {
+  const int np = plan.npasses;
+  if (np > 8) fail(CJ_ERR_UNSUPPORTED, "histogram of more than 8 passes");
+  block_hist(ctx, keys, n, key_bytes, plan, g, cnt_dev, hparts);
+  ctx->kbegin("digit_bases", 12ull * kRadix * np);
+  k_digit_bases<<<1, kRadix, 0, ctx->stream>>>(cnt_dev, g.nblocks, np, totals_dev, base_dev);
+  ctx->kend();
+  CJ_CUDA(cudaGetLastError());
+  if (totals_host) {
+    totals_host->resize((size_t)kRadix * np);
+    CJ_CUDA(cudaMemcpyAsync(ctx->host_pinned, totals_dev, sizeof(uint32_t) * kRadix * np,
                             cudaMemcpyDeviceToHost, ctx->stream));
     CJ_CUDA(cudaStreamSynchronize(ctx->stream));
-    std::memcpy(counts_host->data(), ctx->host_pinned, sizeof(uint32_t) * kRadix * np);
+    std::memcpy(totals_host->data(), ctx->host_pinned, sizeof(uint32_t) * kRadix * np);
   }
 }
 
 void scatter_pass(cj_ctx* ctx, const void* keys_in, void* keys_out, uint64_t n, int key_bytes,
-                  uint32_t lo, uint32_t hi, const uint64_t* base_dev, const ValCols& vals) {
+                  uint32_t lo, uint32_t hi, const uint64_t* base_dev, const uint32_t* cnt,
+                  uint32_t cnt_stride, const ScatterGeom& g, const ValCols& vals, uint32_t hparts) {
   if (n == 0) return;
+  if (hparts && !(g.tma && cnt)) fail(CJ_ERR_UNSUPPORTED, "shard partition needs aligned columns");
+  uint64_t row = key_bytes, wrow = key_bytes;
+  for (int c = 0; c < vals.n; ++c) {
+    row += vals.bytes[c] - ((vals.gen_ids && c == 0) ? 4 : 0);
+    wrow += vals.bytes[c];
+  }
+  if (g.tma && cnt) {
+    BlockPassArgs a{};
+    a.keys_in = keys_in;
+    a.keys_out = keys_out;
+    a.n = n;
+    a.tiles = g.tiles;
+    a.nblocks = g.nblocks;
+    a.shift = lo;
+    a.bits = hi - lo;
+    a.mask = (1u << (hi - lo)) - 1u;
+    a.hparts = hparts;
+    a.base = base_dev;
+    a.cnt = cnt;
+    a.cnt_stride = cnt_stride;
+    a.stage_bytes = g.stage_bytes;
+    a.pbytes = g.pbytes;
+    a.stages = g.stages;
+    a.nvals = vals.n;
+    a.gen_ids = vals.gen_ids;
+    for (int c = 0; c < vals.n; ++c) {
+      a.vin[c] = vals.in[c];
+      a.vout[c] = vals.out[c];
+      a.vbytes[c] = vals.bytes[c];
+      a.voff[c] = g.voff[c];
+    }
+    ctx->kbegin("scatter_pass", n * (row + wrow));
+    if (key_bytes == 4) {
+      if (g.items == 8) launch_blocks<uint32_t, 8>(ctx, a, g.smem);
+      else if (g.items == 4) launch_blocks<uint32_t, 4>(ctx, a, g.smem);
+      else launch_blocks<uint32_t, 2>(ctx, a, g.smem);
+    } else {
+      if (g.items == 8) launch_blocks<uint64_t, 8>(ctx, a, g.smem);
+      else if (g.items == 4) launch_blocks<uint64_t, 4>(ctx, a, g.smem);
+      else launch_blocks<uint64_t, 2>(ctx, a, g.smem);
+    }
+    ctx->kend();
+    CJ_CUDA(cudaGetLastError());
+    return;
+  }
+  // fallback for unaligned columns: register-staged onesweep with look-back
   const int items = key_bytes == 4 ? PassShape<uint32_t>::kItems : PassShape<uint64_t>::kItems;
   const uint64_t tile = (uint64_t)kPassThreads * items;
   const uint64_t tiles = (n + tile - 1) / tile;
@@ -365,11 +749,7 @@ void scatter_pass(cj_ctx* ctx, const void* keys_in, void* keys_out, uint64_t n, 
     a.vout[c] = vals.out[c];
     a.vbytes[c] = vals.bytes[c];
   }
-  uint64_t row = key_bytes;
-  for (int c = 0; c < vals.n; ++c) row += vals.bytes[c] - ((vals.gen_ids && c == 0) ? 4 : 0);
-  uint64_t wrow = key_bytes;
-  for (int c = 0; c < vals.n; ++c) wrow += vals.bytes[c];
-  ctx->kbegin("scatter_pass", n * (row + wrow));
+  ctx->kbegin("scatter_pass_ldg", n * (row + wrow));
   if (key_bytes == 4)
     k_scatter_pass<uint32_t><<<(unsigned)tiles, kPassThreads, 0, ctx->stream>>>(a);
   else
@@ -399,18 +779,22 @@ void copy_columns(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, int
 
 void lsd_partition(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, int key_bytes,
                    const PassPlan& plan, const ValCols& vals, std::vector<uint32_t>* counts_out) {
-  std::vector<uint32_t> counts;
-  Scratch cnt(ctx, sizeof(uint32_t) * kRadix * CJ_MAX_PASSES);
-  Scratch base(ctx, sizeof(uint64_t) * kRadix * CJ_MAX_PASSES);
-  histogram_passes(ctx, keys, n, key_bytes, plan, cnt.as<uint32_t>(), base.as<uint64_t>(),
-                   &counts);
-  if (counts_out) *counts_out = counts;
+  if (plan.npasses > 8) fail(CJ_ERR_UNSUPPORTED, "LSD segment longer than 8 passes");
+  const int np = plan.npasses;
+  const ScatterGeom g0 = scatter_geom(ctx, n, key_bytes, vals, keys);
+  std::vector<uint32_t> totals;
+  Scratch cnt(ctx, sizeof(uint32_t) * kRadix * std::max(np, 1) * g0.nblocks);
+  Scratch tot(ctx, sizeof(uint32_t) * kRadix * std::max(np, 1));
+  Scratch base(ctx, sizeof(uint64_t) * kRadix * std::max(np, 1));
+  histogram_passes(ctx, keys, n, key_bytes, plan, g0, cnt.as<uint32_t>(), tot.as<uint32_t>(),
+                   base.as<uint64_t>(), &totals);
+  if (counts_out) *counts_out = totals;
   std::vector<int> live;
-  for (int p = 0; p < plan.npasses; ++p) {
+  for (int p = 0; p < np; ++p) {
     if (plan.hi[p] == plan.lo[p]) continue;
     bool constant = n == 0;
     for (int d = 0; d < kRadix && !constant; ++d)
-      if (counts[(size_t)p * kRadix + d] == n) constant = true;
+      if (totals[(size_t)p * kRadix + d] == n) constant = true;
     if (!constant) live.push_back(p);
   }
   if (live.empty()) {
@@ -420,10 +804,9 @@ void lsd_partition(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, in
   // ping-pong scratch; the first target is chosen so the last pass lands in
   // the caller's buffers (primitives.cpp:236-255)
   const int nv = vals.n;
-  Scratch sk(ctx, live.size() > 1 ? n * key_bytes : 0);
-  std::vector<Scratch*> sv;
+  Scratch sk(ctx, live.size() > 1 ? n * key_bytes + kPad : 0);
   uint64_t vbytes_total = 0;
-  auto col_span = [&](int c) { return (n * vals.bytes[c] + 255) & ~uint64_t(255); };
+  auto col_span = [&](int c) { return (n * vals.bytes[c] + kPad + 255) & ~uint64_t(255); };
   for (int c = 0; c < nv; ++c) vbytes_total += col_span(c);
   Scratch svals(ctx, live.size() > 1 ? vbytes_total : 0);
   void* scratch_cols[CJ_MAX_COLS + 1] = {};
@@ -434,6 +817,7 @@ void lsd_partition(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, in
       off += col_span(c);
     }
   }
+  Scratch cnt2(ctx, live.size() > 1 ? sizeof(uint32_t) * kRadix * g0.nblocks + 4096 : 0);
   const void* cur_k = keys;
   ValCols cur = vals;
   bool to_out = (live.size() % 2) == 1;
@@ -443,13 +827,54 @@ void lsd_partition(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, in
     void* tk = to_out ? keys_out : sk.p;
     for (int c = 0; c < nv; ++c) step.out[c] = to_out ? vals.out[c] : scratch_cols[c];
     step.gen_ids = li == 0 ? vals.gen_ids : 0;
-    scatter_pass(ctx, cur_k, tk, n, key_bytes, plan.lo[p], plan.hi[p],
-                 base.as<uint64_t>() + (size_t)p * kRadix, step);
+    const uint64_t* pbase = base.as<uint64_t>() + (size_t)p * kRadix;
+    if (li == 0) {
+      scatter_pass(ctx, cur_k, tk, n, key_bytes, plan.lo[p], plan.hi[p], pbase,
+                   g0.tma ? cnt.as<uint32_t>() + (size_t)p * kRadix : nullptr,
+                   (uint32_t)(kRadix * np), g0, step);
+    } else {
+      const ScatterGeom g = scatter_geom(ctx, n, key_bytes, step, cur_k);
+      const uint32_t* pc = nullptr;
+      if (g.tma) {
+        PassPlan one;
+        one.npasses = 1;
+        one.lo[0] = plan.lo[p];
+        one.hi[0] = plan.hi[p];
+        if ((size_t)g.nblocks * kRadix * 4 > (size_t)kRadix * g0.nblocks * 4 + 4096)
+          fail(CJ_ERR_CUDA, "block count scratch too small");
+        block_hist(ctx, cur_k, n, key_bytes, one, g, cnt2.as<uint32_t>());
+        pc = cnt2.as<uint32_t>();
+      }
+      scatter_pass(ctx, cur_k, tk, n, key_bytes, plan.lo[p], plan.hi[p], pbase, pc, kRadix, g,
+                   step);
+    }
     cur_k = tk;
     for (int c = 0; c < nv; ++c) cur.in[c] = step.out[c];
     cur.gen_ids = 0;
     to_out = !to_out;
   }
+}
+
+void shard_partition(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, int key_bytes,
+                     uint32_t parts, const ValCols& vals, uint64_t* counts_host) {
+  if (parts == 0 || parts > 256) fail(CJ_ERR_SPEC_INVALID, "shard count must be in [1, 256]");
+  uint32_t bits = 0;
+  while ((1u << bits) < parts) ++bits;
+  PassPlan plan;
+  plan.npasses = 1;
+  plan.lo[0] = 0;
+  plan.hi[0] = std::max(bits, 1u);
+  const ScatterGeom g = scatter_geom(ctx, n, key_bytes, vals, keys);
+  Scratch cnt(ctx, sizeof(uint32_t) * kRadix * g.nblocks), tot(ctx, sizeof(uint32_t) * kRadix),
+      base(ctx, sizeof(uint64_t) * kRadix);
+  std::vector<uint32_t> totals;
+  histogram_passes(ctx, keys, n, key_bytes, plan, g, cnt.as<uint32_t>(), tot.as<uint32_t>(),
+                   base.as<uint64_t>(), &totals, parts);
+  if (n > 0)
+    scatter_pass(ctx, keys, keys_out, n, key_bytes, 0, plan.hi[0], base.as<uint64_t>(),
+                 cnt.as<uint32_t>(), kRadix, g, vals, parts);
+  for (uint32_t d = 0; d < parts; ++d) counts_host[d] = totals[d];
+  CJ_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
 void partition_offsets(cj_ctx* ctx, const void* keys_sorted, uint64_t n, int key_bytes,
