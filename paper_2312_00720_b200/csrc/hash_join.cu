@@ -425,8 +425,8 @@ __global__ void k_phj_desc(const uint64_t* __restrict__ boff, const uint64_t* __
 template <class K, bool WRITE>
 __global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constant__ FindArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
-  uint16_t* tab = reinterpret_cast<uint16_t*>(smem + (size_t)a.stages * a.stage_bytes);
-  uint32_t* res = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(tab) + 2 * (size_t)a.cap_entries);
+  uint32_t* tab = reinterpret_cast<uint32_t*>(smem + (size_t)a.stages * a.stage_bytes);
+  uint32_t* res = tab + a.cap_entries;
   __shared__ UnitDesc s_desc[2];
   __shared__ __align__(8) uint64_t mbar[2];
   __shared__ uint64_t s_wcount[kTmaWarps], s_wbase[kTmaWarps];
@@ -495,7 +495,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constan
     uint32_t cap_log2 = 1;
     while ((1u << cap_log2) < 2 * nb) ++cap_log2;
     const uint32_t cap = 1u << cap_log2, cmask = cap - 1;
-    for (uint32_t i = tid; i < cap; i += kTmaThreads) tab[i] = kEmpty16;
+    for (uint32_t i = tid; i < cap; i += kTmaThreads) tab[i] = kNoMatch;
     uint8_t* st = smem + (size_t)b * a.stage_bytes;
     const K* bk = reinterpret_cast<const K*>(st + a.off_bk) + (inf.b_lo - dev::align_lo(inf.b_lo, kb));
     const K* pk = reinterpret_cast<const K*>(st + a.off_pk) + (inf.q_lo - dev::align_lo(inf.q_lo, kb));
@@ -509,8 +509,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constan
       const K k = bk[i];
       uint32_t sl = slot_of(k, cap_log2);
       while (true) {
-        const uint16_t old = atomicCAS(&tab[sl], kEmpty16, (uint16_t)i);
-        if (old == kEmpty16) break;
+        const uint32_t old = atomicCAS(&tab[sl], kNoMatch, i);
+        if (old == kNoMatch) break;
         if (bk[old] == k) dup = true;
         sl = (sl + 1) & cmask;
       }
@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constan
     if (__syncthreads_or(dup)) s_dup = 1;
     __syncthreads();
     const bool has_dup = s_dup != 0;
-    uint16_t* sidx = tab;
+    uint16_t* sidx = reinterpret_cast<uint16_t*>(tab);
     if (has_dup) {  // stably sorted chunk positions: bitonic over (key, position)
       uint32_t np2 = 1;
       while (np2 < nb) np2 <<= 1;
@@ -555,8 +555,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constan
         if (!has_dup) {
           uint32_t sl = slot_of(k, cap_log2);
           while (true) {
-            const uint16_t e = tab[sl];
-            if (e == kEmpty16) break;
+            const uint32_t e = tab[sl];
+            if (e == kNoMatch) break;
             if (bk[e] == k) { out = e; m = 1; break; }
             sl = (sl + 1) & cmask;
           }
@@ -696,7 +696,7 @@ bool tma_layout(FindArgs& a, size_t* smem_out) {
   }
   a.stage_bytes = (uint32_t)off;
   a.cap_entries = 1u << a.cap_log2;
-  const size_t smem = (size_t)a.stages * off + up(2 * (size_t)a.cap_entries) + (size_t)a.qchunk * 4;
+  const size_t smem = (size_t)a.stages * off + up(4 * (size_t)a.cap_entries) + (size_t)a.qchunk * 4;
   *smem_out = smem;
   return smem <= 210 * 1024;
 }

@@ -345,7 +345,7 @@ struct BlockPassArgs {
 };
 
 template <class K, int ITEMS>
-__global__ void __launch_bounds__(kTmaThreads, 2)
+__global__ void __launch_bounds__(kTmaThreads, 1)
 k_scatter_blocks(const __grid_constant__ BlockPassArgs a) {
   constexpr uint32_t kTile = ITEMS * kTmaThreads;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -605,10 +605,10 @@ ScatterGeom scatter_geom(cj_ctx* ctx, uint64_t n, int key_bytes, const ValCols& 
   const char* e_items = std::getenv("CJ_SCATTER_ITEMS");
   const char* e_ctas = std::getenv("CJ_SCATTER_CTAS");
   const char* e_stages = std::getenv("CJ_SCATTER_STAGES");
-  const int want_items = e_items ? std::atoi(e_items) : 4;
-  g.ctas_per_sm = e_ctas ? std::max(1, std::atoi(e_ctas)) : 2;
+  const int want_items = e_items ? std::atoi(e_items) : 8;
+  g.ctas_per_sm = e_ctas ? std::max(1, std::atoi(e_ctas)) : 1;
   g.stages = e_stages ? std::min(2, std::max(1, std::atoi(e_stages))) : 2;
-  const size_t budget = (g.ctas_per_sm >= 2 ? 100 : 200) * 1024;
+  const size_t budget = (g.ctas_per_sm >= 2 ? 100 : 210) * 1024;
   for (int items : {8, 4, 2}) {
     if (items > want_items && items > 2) continue;
     g.items = items;
