@@ -196,19 +196,37 @@ def main():
     ctx = cj.Context(local)
     algo, pattern = a.variant.split("-")
     nr, ns = R_ROWS >> a.scale_log2, S_ROWS >> a.scale_log2
-    R, S = cj.gen_pk_fk(ctx, nr, ns, NPAY, NPAY, 4, 4, 1.0, 0.0, SEED + rank)
-    Rc, Sc = cj.coljoin.c_relation(R), cj.coljoin.c_relation(S)
-    opt = cj.options(algo, pattern)
     res = A.JoinResult()
     L = A.lib()
+    opt = cj.options(algo, pattern)
+    shuffle = {"exchange_ms": 0.0, "bytes": 0}
+    if world == 1:
+        # headline config: inputs bit-identical to the reference generator
+        R, S = cj.gen_pk_fk(ctx, nr, ns, NPAY, NPAY, 4, 4, 1.0, 0.0, SEED)
+        Rc, Sc = cj.coljoin.c_relation(R), cj.coljoin.c_relation(S)
 
-    def step():
-        A.check(L.cj_run_join(ctx.h, C.byref(Rc), C.byref(Sc), C.byref(opt), C.byref(res)),
-                ctx.h, "run_join")
-        rows = res.rows
-        phases = (res.transform_ns, res.find_ns, res.materialize_ns)
-        A.check(L.cj_result_free(ctx.h, C.byref(res)), ctx.h, "free")
-        return rows, phases
+        def step():
+            A.check(L.cj_run_join(ctx.h, C.byref(Rc), C.byref(Sc), C.byref(opt), C.byref(res)),
+                    ctx.h, "run_join")
+            rows = res.rows
+            phases = (res.transform_ns, res.find_ns, res.materialize_ns)
+            A.check(L.cj_result_free(ctx.h, C.byref(res)), ctx.h, "free")
+            return rows, phases
+    else:
+        # weak scaling: every rank owns a C2-sized slice of a world-times larger
+        # PK-FK join; rows are shuffled to their key's shard over NCCL
+        from paper_2312_00720_b200 import distributed as D
+        R, S = D.gen_shard(ctx, nr * world, ns * world, rank, world, NPAY, NPAY, SEED)
+
+        def step():
+            t = {}
+            out = D.distributed_join(ctx, R, S, algo, pattern, timings=t)
+            shuffle["exchange_ms"] += t["exchange_ms"]
+            shuffle["bytes"] += t["bytes_sent"]
+            rows = out.matches
+            phases = (out.report.transform_ns, out.report.find_ns, out.report.materialize_ns)
+            del out
+            return rows, phases
 
     for _ in range(a.warmup):
         rows, _ = step()
@@ -236,6 +254,17 @@ def main():
         dist.barrier()
         ms = float(t.item())
     clk = clocks.stop()
+    shuffle_info = None
+    if world > 1:
+        ex = torch.tensor([shuffle["exchange_ms"] / max(a.steps + a.warmup, 1)], device="cuda")
+        dist.all_reduce(ex, op=dist.ReduceOp.MAX)
+        per_step_bytes = shuffle["bytes"] / max(a.steps + a.warmup, 1)
+        shuffle_info = {"bytes_sent_per_gpu_per_step": per_step_bytes,
+                        "exchange_ms_max_over_ranks": float(ex.item()),
+                        "nvlink_gbs_per_gpu": per_step_bytes / 1e9 / (float(ex.item()) / 1e3)
+                        if ex.item() > 0 else None,
+                        "nvlink_peak_gbs_per_dir": 770.0,
+                        "transport": "NCCL all_to_all_single (torch.distributed, backend nccl)"}
     # per-kernel records of the timed region
     names = (C.c_char_p * 4096)()
     kms = (C.c_float * 4096)()
@@ -291,6 +320,10 @@ def main():
                       "materialize": phase_sum[2] / 1e6 / a.steps},
         "gpu_launches": launches, "clocks": clk, "kernels": kernels,
     }
+    if shuffle_info:
+        out["shuffle"] = shuffle_info
+        out["config"]["workload"] = (f"C5-shaped weak scaling: |R|={world}x2^27, |S|={world}x2^28 "
+                                     "total, 4-byte key + 2 x 4-byte payloads, cj_gen_shard")
     if rank == 0 and world == 1 and not a.no_extras:
         # the other variants (3 timed steps each)
         var = {}

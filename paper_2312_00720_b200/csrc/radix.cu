@@ -353,6 +353,7 @@ k_scatter_blocks(const __grid_constant__ BlockPassArgs a) {
   uint8_t* const P = smem + (size_t)a.stages * a.stage_bytes;
   uint8_t* const sdig = P + a.pbytes;
   __shared__ uint16_t whist[kTmaWarps][kRadix];
+  __shared__ uint32_t match_word[kTmaWarps][kRadix];  // peer masks, zero between rounds
   __shared__ uint32_t dstart[kRadix];
   __shared__ uint64_t run[kRadix];   // next global position of each digit in this block
   __shared__ uint64_t goff[kRadix];
@@ -385,6 +386,7 @@ k_scatter_blocks(const __grid_constant__ BlockPassArgs a) {
     dev::fence_mbar_init();
     if (t_begin < t_end && full_tile(t_begin)) issue(0, t_begin);
   }
+  for (int i = tid; i < kTmaWarps * kRadix; i += kTmaThreads) (&match_word[0][0])[i] = 0;
   // starting cursor of every digit: global base + counts of earlier blocks
   if (tid < kRadix) {
     uint64_t c = a.base[tid];
@@ -426,25 +428,33 @@ k_scatter_blocks(const __grid_constant__ BlockPassArgs a) {
     }
     __syncthreads();
 
-    // 1. stable warp ranking over the warp's contiguous segment
+    // 1. stable warp ranking over the warp's contiguous segment.  Peers (lanes
+    //    holding the same digit in this round) are found by OR-ing lane bits
+    //    into a per-warp, per-digit shared word; the lowest peer bumps the
+    //    warp's digit count for the round.
     const uint32_t wseg = warp * 32 * ITEMS;
     K key[ITEMS];
     uint32_t dig[ITEMS], rank[ITEMS];
+    uint32_t* mm = &match_word[warp][0];
+    const bool full = tile_n == kTile;
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       const uint32_t li = wseg + i * 32 + lane;
-      const bool valid = li < tile_n;
-      const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
+      const bool valid = full || li < tile_n;
       key[i] = skey[li];
-      const uint32_t d = valid ? dev::key_digit(key[i], a.shift, a.mask, a.hparts) : 0u;
-      const uint32_t peers = dev::digit_peers(d, a.bits, vmask);
-      const int leader = peers ? __ffs(peers) - 1 : lane;
+      const uint32_t d = dev::key_digit(key[i], a.shift, a.mask, a.hparts);
+      if (valid) atomicOr(&mm[d], 1u << lane);
+      __syncwarp();
+      const uint32_t peers = valid ? mm[d] : 0u;
+      __syncwarp();
+      const bool leader = valid && (peers & dev::lanemask_lt()) == 0;
       uint32_t old = 0;
-      if (valid && lane == leader) {
+      if (leader) {
         old = whist[warp][d];
         whist[warp][d] = (uint16_t)(old + __popc(peers));
+        mm[d] = 0;
       }
-      old = __shfl_sync(0xffffffffu, old, leader);
+      old = __shfl_sync(0xffffffffu, old, __ffs(peers | (1u << lane)) - 1);
       rank[i] = old + __popc(peers & dev::lanemask_lt());
       dig[i] = valid ? d : (uint32_t)kRadix;
       __syncwarp();
@@ -608,7 +618,7 @@ ScatterGeom scatter_geom(cj_ctx* ctx, uint64_t n, int key_bytes, const ValCols& 
   const int want_items = e_items ? std::atoi(e_items) : 8;
   g.ctas_per_sm = e_ctas ? std::max(1, std::atoi(e_ctas)) : 1;
   g.stages = e_stages ? std::min(2, std::max(1, std::atoi(e_stages))) : 2;
-  const size_t budget = (g.ctas_per_sm >= 2 ? 100 : 210) * 1024;
+  const size_t budget = (g.ctas_per_sm >= 2 ? 80 : 190) * 1024;  // + ~30 KB static
   for (int items : {8, 4, 2}) {
     if (items > want_items && items > 2) continue;
     g.items = items;

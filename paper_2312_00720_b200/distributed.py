@@ -81,16 +81,29 @@ def distributed_join(ctx, build, probe, algo="phj", pattern="gftr", group=None,
     import torch.distributed as dist
     world = dist.get_world_size(group)
     part = partition or (lambda rel, p: shard_partition(ctx, rel, p))
+    cuda = ctx is not None
+    if cuda:
+        import torch
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record()
     t0 = time.perf_counter()
     Rs, rcount = part(build, world)
     Ss, scount = part(probe, world)
     t1 = time.perf_counter()
+    if cuda:
+        ev[1].record()
     Rr, _ = exchange(Rs, rcount, group)
     Sr, _ = exchange(Ss, scount, group)
     t2 = time.perf_counter()
+    if cuda:
+        ev[2].record()
+        ev[2].synchronize()
     if timings is not None:
         timings["partition_s"] = t1 - t0
         timings["exchange_s"] = t2 - t1
+        if cuda:
+            timings["partition_ms"] = ev[0].elapsed_time(ev[1])
+            timings["exchange_ms"] = ev[1].elapsed_time(ev[2])
         sent = sum(c for d, c in enumerate(rcount) if d != dist.get_rank(group))
         sent_s = sum(c for d, c in enumerate(scount) if d != dist.get_rank(group))
         row_r = sum(x.element_size() for x in [build.key] + list(build.payloads))
