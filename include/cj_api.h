@@ -54,7 +54,7 @@ enum { CJ_SMJ = 0, CJ_PHJ = 1, CJ_NPHJ = 2 };   /* JoinAlgo    task.hpp:12 (+ NP
 enum { CJ_GFUR = 0, CJ_GFTR = 1 };              /* JoinPattern task.hpp:13 */
 enum { CJ_IDS_PHYSICAL = 0, CJ_IDS_VIRTUAL = 1 };/* TupleIdSemantics column.hpp:130 */
 
-#define CJ_MAX_COLS 8      /* payload columns per relation side */
+#define CJ_MAX_COLS 16     /* payload columns per relation side */
 #define CJ_MAX_PASSES 8    /* radix passes in one plan (8 x 8 bits = 64-bit key) */
 
 typedef struct cj_ctx cj_ctx;

@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libcoljoin_b200.so")
 CSRC = os.path.join(HERE, "csrc")
 
-CJ_MAX_COLS = 8
+CJ_MAX_COLS = 16
 CJ_MAX_PASSES = 8
 SMJ, PHJ, NPHJ = 0, 1, 2
 GFUR, GFTR = 0, 1

@@ -110,6 +110,7 @@ struct ScatterGeom {
   uint32_t voff[CJ_MAX_COLS + 1] = {};
   bool tma = false;  // all inputs 16-byte aligned (TMA bulk copies)
   int ctas_per_sm = 2, stages = 2;
+  int rank = 0;      // in-warp peer search: 0 atomic-OR masks, 1 ballots
 };
 ScatterGeom scatter_geom(cj_ctx* ctx, uint64_t n, int key_bytes, const ValCols& vals,
                          const void* keys_in);

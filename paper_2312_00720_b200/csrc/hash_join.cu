@@ -490,7 +490,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constan
       s_dup = 0;
     }
     uint64_t unit_base = 0;
-    if (WRITE && tid == 32) unit_base = a.unit_off[u];
+    if (WRITE && tid == 32 && a.unit_off) unit_base = a.unit_off[u];
     const uint32_t nb = (uint32_t)(inf.b_hi - inf.b_lo), nq = (uint32_t)(inf.q_hi - inf.q_lo);
     uint32_t cap_log2 = 1;
     while ((1u << cap_log2) < 2 * nb) ++cap_log2;
@@ -584,7 +584,16 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constan
     if (warp == 1) {
       const uint64_t wc = lane < kTmaWarps ? s_wcount[lane] : 0;
       const uint64_t inc = dev::warp_inclusive_sum(wc);
-      const uint64_t base = __shfl_sync(0xffffffffu, unit_base, 0);
+      uint64_t base;
+      if (WRITE && a.unit_off == nullptr) {
+        // single pass: the unit's output offset by decoupled look-back over
+        // the units in order (every CTA is resident; units are taken in order)
+        const uint64_t tot = __shfl_sync(0xffffffffu, inc, kTmaWarps - 1);
+        base = dev::warp_lookback(a.status, u, tot, a.epoch, a.err);
+        if (lane == 0 && u + 1 == units) *a.total_out = base + tot;
+      } else {
+        base = __shfl_sync(0xffffffffu, unit_base, 0);
+      }
       if (lane < kTmaWarps) s_wbase[lane] = base + inc - wc;
       if (!WRITE && lane == kTmaWarps - 1) a.unit_counts[u] = inc;
     }
@@ -619,6 +628,79 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constan
           static_cast<uint64_t*>(a.s_dst[c])[oo] = reinterpret_cast<const uint64_t*>(st + a.off_s[c])[qsh8 + jl];
       }
     };
+    if (!has_dup) {
+      // 3a. compact the hits in probe order: list[t] = (build idx << 16) | probe idx
+      uint32_t* list = res + a.qchunk;
+      const uint64_t ubase = s_wbase[0];
+      uint32_t o = (uint32_t)(s_wbase[warp] - ubase);
+      for (uint32_t r = r0; r < r1; ++r) {
+        const uint32_t jl = r * 32 + lane;
+        const uint32_t e = jl < nq ? res[jl] : kNoMatch;
+        const bool hit = e != kNoMatch;
+        const uint32_t bal = __ballot_sync(0xffffffffu, hit);
+        if (hit) list[o + __popc(bal & dev::lanemask_lt())] = (e << 16) | jl;
+        o += __popc(bal);
+      }
+      __syncthreads();
+      // 3b. column by column, consecutive threads write consecutive output rows
+      uint32_t cnt = (uint32_t)(s_wbase[kTmaWarps - 1] - ubase + s_wcount[kTmaWarps - 1]);
+      if (ubase + cnt > a.capacity) cnt = ubase < a.capacity ? (uint32_t)(a.capacity - ubase) : 0u;
+      constexpr int kE = 8;
+      for (uint32_t t0 = 0; t0 < cnt; t0 += kE * kTmaThreads) {
+        uint32_t L[kE];
+#pragma unroll
+        for (int k = 0; k < kE; ++k) {
+          const uint32_t t = t0 + tid + k * kTmaThreads;
+          L[k] = t < cnt ? list[t] : 0u;
+        }
+        auto each = [&](auto&& f) {
+#pragma unroll
+          for (int k = 0; k < kE; ++k) {
+            const uint32_t t = t0 + tid + k * kTmaThreads;
+            if (t < cnt) f(ubase + t, L[k] >> 16, L[k] & 0xffffu);
+          }
+        };
+        if (a.key_out) {
+          K* ko = static_cast<K*>(a.key_out);
+          each([&](uint64_t oo, uint32_t, uint32_t jl) { ko[oo] = pk[jl]; });
+        }
+        if (a.ids_r)
+          each([&](uint64_t oo, uint32_t li, uint32_t) {
+            const uint64_t gi = inf.b_lo + li;
+            a.ids_r[oo] = a.carried_r ? a.carried_r[gi] : (uint32_t)gi;
+          });
+        if (a.ids_s)
+          each([&](uint64_t oo, uint32_t, uint32_t jl) {
+            const uint64_t j = inf.q_lo + jl;
+            a.ids_s[oo] = a.carried_s ? a.carried_s[j] : (uint32_t)j;
+          });
+        for (int c = 0; c < a.nr; ++c) {
+          if (a.r_bytes[c] == 4) {
+            const uint32_t* sv = reinterpret_cast<const uint32_t*>(st + a.off_r[c]) + bsh4;
+            uint32_t* dv = static_cast<uint32_t*>(a.r_dst[c]);
+            each([&](uint64_t oo, uint32_t li, uint32_t) { dv[oo] = sv[li]; });
+          } else {
+            const uint64_t* sv = reinterpret_cast<const uint64_t*>(st + a.off_r[c]) + bsh8;
+            uint64_t* dv = static_cast<uint64_t*>(a.r_dst[c]);
+            each([&](uint64_t oo, uint32_t li, uint32_t) { dv[oo] = sv[li]; });
+          }
+        }
+        for (int c = 0; c < a.ns; ++c) {
+          if (a.s_bytes[c] == 4) {
+            const uint32_t* sv = reinterpret_cast<const uint32_t*>(st + a.off_s[c]) + qsh4;
+            uint32_t* dv = static_cast<uint32_t*>(a.s_dst[c]);
+            each([&](uint64_t oo, uint32_t, uint32_t jl) { dv[oo] = sv[jl]; });
+          } else {
+            const uint64_t* sv = reinterpret_cast<const uint64_t*>(st + a.off_s[c]) + qsh8;
+            uint64_t* dv = static_cast<uint64_t*>(a.s_dst[c]);
+            each([&](uint64_t oo, uint32_t, uint32_t jl) { dv[oo] = sv[jl]; });
+          }
+        }
+      }
+      __syncthreads();
+      if (a.stages == 1 && tid == 0) issue_next(0);
+      continue;
+    }
     uint64_t o = s_wbase[warp];
     for (uint32_t r = r0; r < r1; ++r) {
       const uint32_t jl = r * 32 + lane;
@@ -696,7 +778,8 @@ bool tma_layout(FindArgs& a, size_t* smem_out) {
   }
   a.stage_bytes = (uint32_t)off;
   a.cap_entries = 1u << a.cap_log2;
-  const size_t smem = (size_t)a.stages * off + up(4 * (size_t)a.cap_entries) + (size_t)a.qchunk * 4;
+  // + res[qchunk] probe results + list[qchunk] compacted hits
+  const size_t smem = (size_t)a.stages * off + up(4 * (size_t)a.cap_entries) + (size_t)a.qchunk * 8;
   *smem_out = smem;
   return smem <= 210 * 1024;
 }
@@ -720,6 +803,25 @@ uint64_t run_find(cj_ctx* ctx, FindArgs a, uint64_t total_units) {
     // count pass (keys only) -> scan -> fill pass; no inter-CTA waiting
     const uint64_t U = total_units;
     uint64_t total = 0;
+    const char* fm = std::getenv("CJ_FIND_PASSES");
+    if (U > 0 && a.write && fm && std::strcmp(fm, "1") == 0) {
+      // one pass: unit offsets by look-back inside the fill kernel
+      const unsigned grid =
+          (unsigned)std::min<uint64_t>((uint64_t)ctx->num_sms * find_ctas_per_sm(), U);
+      a.unit_off = nullptr;
+      CJ_CUDA(cudaFuncSetAttribute(k_phj_tma<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)tma_smem));
+      ctx->kbegin("phj_find", 0);
+      k_phj_tma<K, true><<<grid, kTmaThreads, tma_smem, ctx->stream>>>(a);
+      ctx->kend();
+      CJ_CUDA(cudaGetLastError());
+      uint64_t* h = reinterpret_cast<uint64_t*>(ctx->host_pinned);
+      CJ_CUDA(cudaMemcpyAsync(h, a.total_out, 8, cudaMemcpyDeviceToHost, ctx->stream));
+      CJ_CUDA(cudaStreamSynchronize(ctx->stream));
+      total = h[0];
+      if (total > a.capacity) atomicOr_host_overflow(ctx);
+      return total;
+    }
     if (U > 0) {
       Scratch counts(ctx, U * 8), offs(ctx, U * 8);
       FindArgs ac = a;
@@ -727,12 +829,16 @@ uint64_t run_find(cj_ctx* ctx, FindArgs a, uint64_t total_units) {
       ac.unit_counts = counts.as<uint64_t>();
       size_t smem_c = 0;
       tma_layout<K>(ac, &smem_c);
+      // the count pass needs little shared memory: two CTAs per SM hide latency
+      const char* ec = std::getenv("CJ_COUNT_CTAS");
+      const unsigned grid_c = (unsigned)std::min<uint64_t>(
+          (uint64_t)ctx->num_sms * (ec ? std::max(1, std::atoi(ec)) : 2), U);
       const unsigned grid =
           (unsigned)std::min<uint64_t>((uint64_t)ctx->num_sms * find_ctas_per_sm(), U);
       CJ_CUDA(cudaFuncSetAttribute(k_phj_tma<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem_c));
       ctx->kbegin("phj_count", (uint64_t)(sizeof(K)) * (a.nb_rows + a.np_rows));
-      k_phj_tma<K, false><<<grid, kTmaThreads, smem_c, ctx->stream>>>(ac);
+      k_phj_tma<K, false><<<grid_c, kTmaThreads, smem_c, ctx->stream>>>(ac);
       ctx->kend();
       scan_counts(ctx, counts.as<uint64_t>(), U, offs.as<uint64_t>(), a.total_out);
       CJ_CUDA(cudaGetLastError());

@@ -39,31 +39,40 @@ constexpr int kHistSub = 4;  // CTAs per static block in the counting kernel
 // the contiguous tile range [b*tiles/nblocks, (b+1)*tiles/nblocks) — the same
 // static ranges the scatter kernel walks — so the counts double as the
 // scatter's cross-block cursors (no look-back).  cnt[b][p][d].
-template <class K>
+struct HistArgs {
+  uint64_t n, tile, tiles;
+  uint32_t nblocks, hparts;
+  uint32_t shift[8], mask[8];
+};
+
+template <class K, int NP, bool SHARD>
 __global__ void __launch_bounds__(kHistThreads)
-k_block_hist(const K* __restrict__ keys, uint64_t n, uint64_t tile, uint64_t tiles,
-             uint32_t nblocks, int npasses, uint4 shifts_lo, uint4 shifts_hi, uint4 masks_lo,
-             uint4 masks_hi, uint32_t hparts, uint32_t* __restrict__ cnt) {
-  extern __shared__ uint32_t sh[];  // [warp][npasses * 256]
-  const uint32_t sh_arr[8] = {shifts_lo.x, shifts_lo.y, shifts_lo.z, shifts_lo.w,
-                              shifts_hi.x, shifts_hi.y, shifts_hi.z, shifts_hi.w};
-  const uint32_t mk_arr[8] = {masks_lo.x, masks_lo.y, masks_lo.z, masks_lo.w,
-                              masks_hi.x, masks_hi.y, masks_hi.z, masks_hi.w};
-  const int width = npasses * kRadix;
-  for (int i = threadIdx.x; i < kHistWarps * width; i += kHistThreads) sh[i] = 0;
+k_block_hist(const K* __restrict__ keys, const __grid_constant__ HistArgs a,
+             uint32_t* __restrict__ cnt) {
+  extern __shared__ uint32_t sh[];  // [warp][NP * 256]
+  constexpr int kWidth = NP * kRadix;
+  for (int i = threadIdx.x; i < kHistWarps * kWidth; i += kHistThreads) sh[i] = 0;
   __syncthreads();
-  uint32_t* mine = sh + (threadIdx.x >> 5) * width;
+  uint32_t* mine = sh + (threadIdx.x >> 5) * kWidth;
   // gridDim.x = nblocks * kHistSub: sub-CTA s of block b counts a quarter of
   // the block's tiles and adds into cnt[b] (zeroed by the caller)
   const uint64_t b = blockIdx.x / kHistSub, sub = blockIdx.x % kHistSub;
-  const uint64_t t0 = b * tiles / nblocks, t1 = (b + 1) * tiles / nblocks;
-  const uint64_t lo = dev::umin64(n, (t0 + sub * (t1 - t0) / kHistSub) * tile);
-  const uint64_t hi = dev::umin64(n, (t0 + (sub + 1) * (t1 - t0) / kHistSub) * tile);
-  auto count = [&](K k) {
+  const uint64_t t0 = b * a.tiles / a.nblocks, t1 = (b + 1) * a.tiles / a.nblocks;
+  const uint64_t lo = dev::umin64(a.n, (t0 + sub * (t1 - t0) / kHistSub) * a.tile);
+  const uint64_t hi = dev::umin64(a.n, (t0 + (sub + 1) * (t1 - t0) / kHistSub) * a.tile);
+  uint32_t shf[NP], msk[NP];
 #pragma unroll
-    for (int p = 0; p < 8; ++p)
-      if (p < npasses)
-        atomicAdd(&mine[p * kRadix + dev::key_digit(k, sh_arr[p], mk_arr[p], hparts)], 1u);
+  for (int p = 0; p < NP; ++p) {
+    shf[p] = a.shift[p];
+    msk[p] = a.mask[p];
+  }
+  auto count = [&](K k) {
+    if (SHARD) {
+      atomicAdd(&mine[(uint32_t)__umul64hi(dev::mix64((uint64_t)k), (uint64_t)a.hparts)], 1u);
+    } else {
+#pragma unroll
+      for (int p = 0; p < NP; ++p) atomicAdd(&mine[p * kRadix + ((uint32_t)(k >> shf[p]) & msk[p])], 1u);
+    }
   };
   constexpr int kVec = 16 / sizeof(K);
   uint64_t i = lo;
@@ -94,11 +103,34 @@ k_block_hist(const K* __restrict__ keys, uint64_t n, uint64_t tile, uint64_t til
   }
   for (uint64_t j = i + threadIdx.x; j < hi; j += kHistThreads) count(keys[j]);
   __syncthreads();
-  for (int d = threadIdx.x; d < width; d += kHistThreads) {
+  for (int d = threadIdx.x; d < kWidth; d += kHistThreads) {
     uint32_t t = 0;
 #pragma unroll
-    for (int w = 0; w < kHistWarps; ++w) t += sh[w * width + d];
-    if (t) atomicAdd(&cnt[b * width + d], t);
+    for (int w = 0; w < kHistWarps; ++w) t += sh[w * kWidth + d];
+    if (t) atomicAdd(&cnt[b * kWidth + d], t);
+  }
+}
+
+template <class K, int NP, bool SHARD>
+void launch_hist(cj_ctx* ctx, const K* keys, const HistArgs& a, uint32_t* cnt) {
+  const size_t smem = sizeof(uint32_t) * kRadix * NP * kHistWarps;
+  CJ_CUDA(cudaFuncSetAttribute(k_block_hist<K, NP, SHARD>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_block_hist<K, NP, SHARD><<<a.nblocks * kHistSub, kHistThreads, smem, ctx->stream>>>(keys, a, cnt);
+}
+
+template <class K>
+void launch_hist_np(cj_ctx* ctx, const K* keys, const HistArgs& a, int np, uint32_t* cnt) {
+  if (a.hparts) return launch_hist<K, 1, true>(ctx, keys, a, cnt);
+  switch (np) {
+    case 1: return launch_hist<K, 1, false>(ctx, keys, a, cnt);
+    case 2: return launch_hist<K, 2, false>(ctx, keys, a, cnt);
+    case 3: return launch_hist<K, 3, false>(ctx, keys, a, cnt);
+    case 4: return launch_hist<K, 4, false>(ctx, keys, a, cnt);
+    case 5: return launch_hist<K, 5, false>(ctx, keys, a, cnt);
+    case 6: return launch_hist<K, 6, false>(ctx, keys, a, cnt);
+    case 7: return launch_hist<K, 7, false>(ctx, keys, a, cnt);
+    default: return launch_hist<K, 8, false>(ctx, keys, a, cnt);
   }
 }
 
@@ -312,15 +344,12 @@ k_scatter_pass(const __grid_constant__ PassArgs a) {
   }
 }
 
-// ---- blocked scatter pass, TMA-pipelined (the default path) ---------------
+// ---- blocked scatter pass: shared types ----------------------------------------
 //
 // Persistent CTAs of 512 threads, one per SM; CTA b walks its static range of
 // consecutive tiles in order and carries the per-digit write cursors in shared
 // memory, so no CTA ever waits for another (the cross-block starting cursors
-// come from the per-block counts of k_block_hist).  While a tile is ranked and
-// written, the next tile's keys and carried columns stream into the other
-// shared-memory stage by cp.async.bulk.  Ranking uses bit ballots; lanes, item
-// rounds and warps are visited in input order, so the pass is stable.
+// come from the per-block counts of k_block_hist).
 
 constexpr int kTmaThreads = 512;
 constexpr int kTmaWarps = kTmaThreads / 32;
@@ -344,19 +373,220 @@ struct BlockPassArgs {
   uint32_t voff[CJ_MAX_COLS + 1];
 };
 
-template <class K, int ITEMS>
-__global__ void __launch_bounds__(kTmaThreads, 1)
-k_scatter_blocks(const __grid_constant__ BlockPassArgs a) {
+// offsets[p] = first index whose low-`bits` digit is >= p (keys sorted by it)
+template <class K>
+__global__ void k_offsets(const K* __restrict__ keys, uint64_t n, uint32_t bits,
+                          uint64_t* __restrict__ off) {
+  const uint64_t fanout = 1ull << bits;
+  const K mask = (K)(fanout - 1);
+  for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p <= fanout;
+       p += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if ((uint64_t)(keys[mid] & mask) < p) lo = mid + 1; else hi = mid;
+    }
+    off[p] = p == fanout ? n : lo;
+  }
+}
+
+// ---- blocked scatter pass v2: source-index staging ---------------------------
+//
+// A tile costs four block barriers regardless of the number of carried columns:
+//   1. rank: each warp ranks its contiguous 32*ITEMS segment (input order =
+//      (warp, item, lane)); the stable in-warp peers of a digit come from
+//      RANK: 0 = shared atomic-OR peer masks (default), 1 = bit ballots;
+//      the lowest peer bumps the warp's per-digit count (no atomics);
+//   2. scan: per digit, exclusive prefix over warps and over digits;
+//   3. place: slot of every row in the digit-sorted tile; only the SOURCE
+//      INDEX (u16) is written to shared memory;
+//   4. write: slot j reads src = sidx[j], the key at src (its digit gives the
+//      run's global offset) and every carried column at src straight from the
+//      TMA stage, and stores them at goff[d] + j.  Consecutive slots of a digit
+//      run are consecutive output rows (coalesced runs), and no column needs a
+//      re-staging barrier.
+// Global row indices are u32 (kMaxRows = 2^31 - 1, column.hpp:21).
+
+template <int RANK>
+__device__ __forceinline__ uint32_t peers_of(uint32_t d, bool valid, uint32_t* mm, uint32_t bits) {
+  const uint32_t lane = threadIdx.x & 31u;
+  if (RANK == 0) {
+    if (valid) atomicOr(&mm[d], 1u << lane);
+    __syncwarp();
+    const uint32_t p = valid ? mm[d] : 0u;
+    __syncwarp();
+    return p;
+  }
+  return dev::digit_peers(d, bits, __ballot_sync(0xffffffffu, valid)) & (valid ? ~0u : 0u);
+}
+
+#ifdef CJ_PHASE_CLOCKS
+// Debug builds only (tools/ubench_phases): cycles per scatter phase, CTA 0 thread 0.
+__device__ unsigned long long g_phase_clk[16];
+#define CJ_CLK(i) CJ_CLKT(i, 0)
+#define CJ_CLKT(i, th)                                              \
+  do {                                                              \
+    if (blockIdx.x == 0 && threadIdx.x == (th)) {                   \
+      const long long now = clock64();                              \
+      g_phase_clk[i] += (unsigned long long)(now - clk_prev);       \
+      clk_prev = now;                                               \
+    }                                                               \
+  } while (0)
+#else
+#define CJ_CLK(i) \
+  do {            \
+  } while (0)
+#define CJ_CLKT(i, th) \
+  do {                 \
+  } while (0)
+#endif
+
+// Digit of key k in pass (shift, mask) or, in shard mode, its shard.
+template <bool SHARD, class K>
+__device__ __forceinline__ uint32_t digit_of(K k, const BlockPassArgs& a) {
+  if (SHARD) return (uint32_t)__umul64hi(dev::mix64((uint64_t)k), (uint64_t)a.hparts);
+  return (uint32_t)(k >> a.shift) & a.mask;
+}
+
+// One tile of k_scatter_v2 (phases 1-4).  FULL: tile_n == kTile, no guards.
+template <class K, int ITEMS, int RANK, bool SHARD, bool FULL>
+__device__ __forceinline__ void scatter_tile(const BlockPassArgs& a, const uint8_t* st,
+                                             uint16_t* sidx, uint16_t (*whist)[kRadix],
+                                             uint32_t* mm, uint32_t* dstart, uint32_t* run,
+                                             uint32_t* goff, uint32_t* wsum, uint32_t tbase,
+                                             uint32_t tile_n) {
+  constexpr uint32_t kTile = ITEMS * kTmaThreads;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const K* skey = reinterpret_cast<const K*>(st);
+#ifdef CJ_PHASE_CLOCKS
+  long long clk_prev = clock64();
+#endif
+
+  // 1. stable in-warp ranking; pk = (rank within warp << 8) | digit, or ~0u
+  const uint32_t wseg = warp * 32 * ITEMS;
+  uint32_t pk[ITEMS];
+  uint16_t* wh = &whist[warp][0];
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const uint32_t li = wseg + i * 32 + lane;
+    const bool valid = FULL || li < tile_n;
+    const uint32_t d = digit_of<SHARD>(skey[li], a);
+    const uint32_t peers = peers_of<RANK>(d, valid, mm, a.bits);
+    const uint32_t lt = peers & dev::lanemask_lt();
+    uint32_t old = 0;
+    if (valid && lt == 0) {
+      old = wh[d];
+      wh[d] = (uint16_t)(old + __popc(peers));
+      if (RANK == 0) mm[d] = 0;
+    }
+    old = __shfl_sync(0xffffffffu, old, __ffs(peers | (1u << lane)) - 1);
+    pk[i] = valid ? ((old + __popc(lt)) << 8) | d : 0xffffffffu;
+    if (RANK == 0) __syncwarp();
+  }
+  __syncthreads();
+  CJ_CLK(0);
+
+  // 2. per digit: tile total, exclusive digit start, then whist[w][d] = slot
+  //    of warp w's first row of digit d (digit start + earlier warps' counts)
+  {
+    uint32_t c[kTmaWarps], r = 0, inc = 0;
+    if (tid < kRadix) {
+#pragma unroll
+      for (int w = 0; w < kTmaWarps; ++w) {
+        c[w] = whist[w][tid];
+        r += c[w];
+      }
+      inc = dev::warp_inclusive_sum(r);
+      if (lane == 31) wsum[warp] = inc;
+    }
+    __syncthreads();
+    CJ_CLK(2);
+    if (tid < kRadix) {
+      uint32_t off = 0;
+#pragma unroll
+      for (int w = 0; w < kRadix / 32; ++w) off += w < warp ? wsum[w] : 0;
+      const uint32_t ds = off + inc - r;
+      uint32_t p = ds;
+#pragma unroll
+      for (int w = 0; w < kTmaWarps; ++w) {
+        whist[w][tid] = (uint16_t)p;
+        p += c[w];
+      }
+      goff[tid] = run[tid] - ds;
+      run[tid] += r;
+    }
+    __syncthreads();
+    CJ_CLK(3);
+  }
+
+  // 3. slot of every row; record its source index
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    if (FULL || pk[i] != 0xffffffffu) {
+      sidx[wh[pk[i] & 0xffu] + (pk[i] >> 8)] = (uint16_t)(wseg + i * 32 + lane);
+    }
+  }
+  __syncthreads();
+  CJ_CLK(1);
+
+  // 4. write key + carried columns of each slot (loads batched for ILP)
+  uint32_t src[ITEMS], g[ITEMS];
+  K key[ITEMS];
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    const uint32_t j = tid + k * kTmaThreads;
+    src[k] = (FULL || j < tile_n) ? sidx[j] : 0u;
+  }
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) key[k] = skey[src[k]];
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) g[k] = goff[digit_of<SHARD>(key[k], a)] + tid + k * kTmaThreads;
+  K* __restrict__ kout = static_cast<K*>(a.keys_out);
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k)
+    if (FULL || tid + k * kTmaThreads < tile_n) kout[g[k]] = key[k];
+  for (int c = 0; c < a.nvals; ++c) {
+    if (a.gen_ids && c == 0) {
+      uint32_t* __restrict__ vout = static_cast<uint32_t*>(a.vout[c]);
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k)
+        if (FULL || tid + k * kTmaThreads < tile_n) vout[g[k]] = tbase + src[k];
+    } else if (a.vbytes[c] == 4) {
+      const uint32_t* sv = reinterpret_cast<const uint32_t*>(st + a.voff[c]);
+      uint32_t* __restrict__ vout = static_cast<uint32_t*>(a.vout[c]);
+      uint32_t v[ITEMS];
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) v[k] = sv[src[k]];
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k)
+        if (FULL || tid + k * kTmaThreads < tile_n) vout[g[k]] = v[k];
+    } else {
+      const uint64_t* sv = reinterpret_cast<const uint64_t*>(st + a.voff[c]);
+      uint64_t* __restrict__ vout = static_cast<uint64_t*>(a.vout[c]);
+      uint64_t v[ITEMS];
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) v[k] = sv[src[k]];
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k)
+        if (FULL || tid + k * kTmaThreads < tile_n) vout[g[k]] = v[k];
+    }
+  }
+  CJ_CLK(7);
+  (void)kTile;
+}
+
+template <class K, int ITEMS, int RANK, bool SHARD, int MINB>
+__global__ void __launch_bounds__(kTmaThreads, MINB)
+k_scatter_v2(const __grid_constant__ BlockPassArgs a) {
   constexpr uint32_t kTile = ITEMS * kTmaThreads;
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* const stage0 = smem;
-  uint8_t* const P = smem + (size_t)a.stages * a.stage_bytes;
-  uint8_t* const sdig = P + a.pbytes;
+  uint16_t* const sidx = reinterpret_cast<uint16_t*>(smem + (size_t)a.stages * a.stage_bytes);
   __shared__ uint16_t whist[kTmaWarps][kRadix];
-  __shared__ uint32_t match_word[kTmaWarps][kRadix];  // peer masks, zero between rounds
+  __shared__ uint32_t match_word[RANK == 0 ? kTmaWarps : 1][kRadix];
   __shared__ uint32_t dstart[kRadix];
-  __shared__ uint64_t run[kRadix];   // next global position of each digit in this block
-  __shared__ uint64_t goff[kRadix];
+  __shared__ uint32_t run[kRadix];   // next global row of each digit in this block
+  __shared__ uint32_t goff[kRadix];  // global row of tile slot 0 of each digit's run (mod 2^32)
   __shared__ uint32_t wsum[kRadix / 32];
   __shared__ __align__(8) uint64_t mbar[2];
 
@@ -386,30 +616,39 @@ k_scatter_blocks(const __grid_constant__ BlockPassArgs a) {
     dev::fence_mbar_init();
     if (t_begin < t_end && full_tile(t_begin)) issue(0, t_begin);
   }
-  for (int i = tid; i < kTmaWarps * kRadix; i += kTmaThreads) (&match_word[0][0])[i] = 0;
-  // starting cursor of every digit: global base + counts of earlier blocks
+  if (RANK == 0)
+    for (int i = tid; i < kTmaWarps * kRadix; i += kTmaThreads) (&match_word[0][0])[i] = 0;
   if (tid < kRadix) {
     uint64_t c = a.base[tid];
     for (uint64_t b2 = 0; b2 < blk; ++b2) c += a.cnt[b2 * a.cnt_stride + tid];
-    run[tid] = c;
+    run[tid] = (uint32_t)c;
   }
   __syncthreads();
 
-  uint32_t phase[2] = {0, 0};
+  uint32_t ph0 = 0, ph1 = 0;
   int b = 0;
+  uint32_t* mm = &match_word[RANK == 0 ? warp : 0][0];
   for (uint64_t t = t_begin; t < t_end; ++t, b = (b + 1) % a.stages) {
     if (a.stages == 2 && tid == 0 && t + 1 < t_end && full_tile(t + 1)) {
       dev::fence_proxy_async();
       issue(b ^ 1, t + 1);
     }
-    for (int i = tid; i < kTmaWarps * kRadix; i += kTmaThreads) (&whist[0][0])[i] = 0;
+    // each warp zeroes its own histogram row (only it touches the row until
+    // the barrier after ranking)
+    {
+      uint32_t* wrow = reinterpret_cast<uint32_t*>(&whist[warp][0]);
+#pragma unroll
+      for (int i = 0; i < kRadix / 2 / 32; ++i) wrow[lane + 32 * i] = 0;
+      __syncwarp();
+    }
     const uint64_t tbase = t * kTile;
     const uint32_t tile_n = (uint32_t)dev::umin64(kTile, a.n - tbase);
     uint8_t* st = stage0 + (size_t)b * a.stage_bytes;
-    const K* skey = reinterpret_cast<const K*>(st);
     if (full_tile(t)) {
-      dev::mbar_wait(&mbar[b], phase[b]);
-      phase[b] ^= 1;
+      dev::mbar_wait(&mbar[b], b ? ph1 : ph0);
+      if (b) ph1 ^= 1; else ph0 ^= 1;
+      scatter_tile<K, ITEMS, RANK, SHARD, true>(a, st, sidx, whist, mm, dstart, run, goff, wsum,
+                                                (uint32_t)tbase, tile_n);
     } else {  // last, partial tile: plain loads
       K* wk = reinterpret_cast<K*>(st);
       for (uint32_t j = tid; j < kTile; j += kTmaThreads) wk[j] = j < tile_n ? kin[tbase + j] : K(0);
@@ -425,128 +664,9 @@ k_scatter_blocks(const __grid_constant__ BlockPassArgs a) {
           for (uint32_t j = tid; j < tile_n; j += kTmaThreads) dst[j] = src[j];
         }
       }
-    }
-    __syncthreads();
-
-    // 1. stable warp ranking over the warp's contiguous segment.  Peers (lanes
-    //    holding the same digit in this round) are found by OR-ing lane bits
-    //    into a per-warp, per-digit shared word; the lowest peer bumps the
-    //    warp's digit count for the round.
-    const uint32_t wseg = warp * 32 * ITEMS;
-    K key[ITEMS];
-    uint32_t dig[ITEMS], rank[ITEMS];
-    uint32_t* mm = &match_word[warp][0];
-    const bool full = tile_n == kTile;
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      const uint32_t li = wseg + i * 32 + lane;
-      const bool valid = full || li < tile_n;
-      key[i] = skey[li];
-      const uint32_t d = dev::key_digit(key[i], a.shift, a.mask, a.hparts);
-      if (valid) atomicOr(&mm[d], 1u << lane);
-      __syncwarp();
-      const uint32_t peers = valid ? mm[d] : 0u;
-      __syncwarp();
-      const bool leader = valid && (peers & dev::lanemask_lt()) == 0;
-      uint32_t old = 0;
-      if (leader) {
-        old = whist[warp][d];
-        whist[warp][d] = (uint16_t)(old + __popc(peers));
-        mm[d] = 0;
-      }
-      old = __shfl_sync(0xffffffffu, old, __ffs(peers | (1u << lane)) - 1);
-      rank[i] = old + __popc(peers & dev::lanemask_lt());
-      dig[i] = valid ? d : (uint32_t)kRadix;
-      __syncwarp();
-    }
-    __syncthreads();
-
-    // 2. per digit: exclusive prefix over warps and tile total; digit starts
-    uint32_t tile_count = 0, inc = 0;
-    if (tid < kRadix) {
-      uint32_t r = 0;
-#pragma unroll
-      for (int w = 0; w < kTmaWarps; ++w) {
-        const uint32_t c = whist[w][tid];
-        whist[w][tid] = (uint16_t)r;
-        r += c;
-      }
-      tile_count = r;
-      inc = dev::warp_inclusive_sum(tile_count);
-      if (lane == 31) wsum[warp] = inc;
-    }
-    __syncthreads();
-    if (tid < kRadix) {
-      uint32_t off = 0;
-#pragma unroll
-      for (int w = 0; w < kRadix / 32; ++w) off += w < warp ? wsum[w] : 0;
-      const uint32_t ds = off + inc - tile_count;
-      dstart[tid] = ds;
-      goff[tid] = run[tid] - ds;
-      run[tid] += tile_count;
-    }
-    __syncthreads();
-
-    // 3. keys to their tile-local sorted slots
-    uint32_t lpos[ITEMS];
-    K* pk = reinterpret_cast<K*>(P);
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      if (dig[i] < kRadix) {
-        lpos[i] = dstart[dig[i]] + whist[warp][dig[i]] + rank[i];
-        pk[lpos[i]] = key[i];
-        sdig[lpos[i]] = (uint8_t)dig[i];
-      } else {
-        lpos[i] = 0xffffffffu;
-      }
-    }
-    __syncthreads();
-
-    // 4. write keys digit-run by digit-run; remember each slot's destination
-    uint64_t gpos[ITEMS];
-    K* __restrict__ kout = static_cast<K*>(a.keys_out);
-#pragma unroll
-    for (int k = 0; k < ITEMS; ++k) {
-      const uint32_t j = tid + k * kTmaThreads;
-      if (j < tile_n) {
-        gpos[k] = goff[sdig[j]] + j;
-        kout[gpos[k]] = pk[j];
-      }
-    }
-
-    // 5. every carried column through the same permutation
-    for (int c = 0; c < a.nvals; ++c) {
-      const bool gen = a.gen_ids && c == 0;
       __syncthreads();
-      if (a.vbytes[c] == 4) {
-        uint32_t* pv = reinterpret_cast<uint32_t*>(P);
-        const uint32_t* sv = reinterpret_cast<const uint32_t*>(st + a.voff[c]);
-#pragma unroll
-        for (int i = 0; i < ITEMS; ++i)
-          if (lpos[i] != 0xffffffffu)
-            pv[lpos[i]] = gen ? (uint32_t)(tbase + wseg + i * 32 + lane) : sv[wseg + i * 32 + lane];
-        __syncthreads();
-        uint32_t* __restrict__ vout = static_cast<uint32_t*>(a.vout[c]);
-#pragma unroll
-        for (int k = 0; k < ITEMS; ++k) {
-          const uint32_t j = tid + k * kTmaThreads;
-          if (j < tile_n) vout[gpos[k]] = pv[j];
-        }
-      } else {
-        uint64_t* pv = reinterpret_cast<uint64_t*>(P);
-        const uint64_t* sv = reinterpret_cast<const uint64_t*>(st + a.voff[c]);
-#pragma unroll
-        for (int i = 0; i < ITEMS; ++i)
-          if (lpos[i] != 0xffffffffu)
-            pv[lpos[i]] = gen ? (uint64_t)(tbase + wseg + i * 32 + lane) : sv[wseg + i * 32 + lane];
-        __syncthreads();
-        uint64_t* __restrict__ vout = static_cast<uint64_t*>(a.vout[c]);
-#pragma unroll
-        for (int k = 0; k < ITEMS; ++k) {
-          const uint32_t j = tid + k * kTmaThreads;
-          if (j < tile_n) vout[gpos[k]] = pv[j];
-        }
-      }
+      scatter_tile<K, ITEMS, RANK, SHARD, false>(a, st, sidx, whist, mm, dstart, run, goff, wsum,
+                                                 (uint32_t)tbase, tile_n);
     }
     __syncthreads();
     if (a.stages == 1 && tid == 0 && t + 1 < t_end && full_tile(t + 1)) {
@@ -556,27 +676,21 @@ k_scatter_blocks(const __grid_constant__ BlockPassArgs a) {
   }
 }
 
-template <class K, int ITEMS>
-void launch_blocks(cj_ctx* ctx, const BlockPassArgs& a, size_t smem) {
-  auto kern = k_scatter_blocks<K, ITEMS>;
+template <class K, int ITEMS, int RANK, int MINB>
+void launch_v2(cj_ctx* ctx, const BlockPassArgs& a, size_t smem) {
+  auto kern = a.hparts ? k_scatter_v2<K, ITEMS, RANK, true, MINB>
+                       : k_scatter_v2<K, ITEMS, RANK, false, MINB>;
   CJ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<a.nblocks, kTmaThreads, smem, ctx->stream>>>(a);
 }
 
-// offsets[p] = first index whose low-`bits` digit is >= p (keys sorted by it)
-template <class K>
-__global__ void k_offsets(const K* __restrict__ keys, uint64_t n, uint32_t bits,
-                          uint64_t* __restrict__ off) {
-  const uint64_t fanout = 1ull << bits;
-  const K mask = (K)(fanout - 1);
-  for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p <= fanout;
-       p += (uint64_t)gridDim.x * blockDim.x) {
-    uint64_t lo = 0, hi = n;
-    while (lo < hi) {
-      const uint64_t mid = (lo + hi) >> 1;
-      if ((uint64_t)(keys[mid] & mask) < p) lo = mid + 1; else hi = mid;
-    }
-    off[p] = p == fanout ? n : lo;
+template <class K, int RANK>
+void launch_v2_items(cj_ctx* ctx, const BlockPassArgs& a, size_t smem, int items) {
+  switch (items) {
+    case 16: launch_v2<K, 16, RANK, 1>(ctx, a, smem); break;
+    case 12: launch_v2<K, 12, RANK, 1>(ctx, a, smem); break;
+    case 8: launch_v2<K, 8, RANK, 1>(ctx, a, smem); break;
+    default: launch_v2<K, 4, RANK, 1>(ctx, a, smem); break;
   }
 }
 
@@ -613,21 +727,25 @@ ScatterGeom scatter_geom(cj_ctx* ctx, uint64_t n, int key_bytes, const ValCols& 
   g.tma = al && !(mode && std::strcmp(mode, "ldg") == 0);
   // tuning knobs (defaults chosen from the sweeps recorded in profiles/)
   const char* e_items = std::getenv("CJ_SCATTER_ITEMS");
-  const char* e_ctas = std::getenv("CJ_SCATTER_CTAS");
   const char* e_stages = std::getenv("CJ_SCATTER_STAGES");
-  const int want_items = e_items ? std::atoi(e_items) : 8;
-  g.ctas_per_sm = e_ctas ? std::max(1, std::atoi(e_ctas)) : 1;
+  const char* e_rank = std::getenv("CJ_RANK");
+  g.rank = e_rank ? std::atoi(e_rank) : 0;
+  g.ctas_per_sm = 1;  // (2 CTAs/SM with single stages measured slower: profiles/)
   g.stages = e_stages ? std::min(2, std::max(1, std::atoi(e_stages))) : 2;
-  const size_t budget = (g.ctas_per_sm >= 2 ? 80 : 190) * 1024;  // + ~30 KB static
-  for (int items : {8, 4, 2}) {
-    if (items > want_items && items > 2) continue;
+  const int want_items = e_items ? std::atoi(e_items) : 12;
+  // 227 KB per CTA minus the static arrays (whist 8 KB, match words 16 KB for
+  // rank mode 0, ~3 KB of cursors)
+  const size_t budget = (size_t)(227 - (g.rank == 0 ? 28 : 12)) * 1024;
+  for (int items : {16, 12, 8, 4}) {
+    if (items > want_items && items > 4) continue;
     g.items = items;
     g.tile = (uint64_t)kTmaThreads * items;
     g.stage_bytes = (uint32_t)(g.tile * row);
-    g.pbytes = (uint32_t)(g.tile * maxw);
-    g.smem = (size_t)g.stages * g.stage_bytes + g.pbytes + g.tile;
+    g.pbytes = 0;
+    g.smem = (size_t)g.stages * g.stage_bytes + g.tile * 2;
     if (g.smem <= budget) break;
   }
+  if (g.smem > budget) g.tma = false;  // rows too wide: the look-back onesweep path
   uint32_t off = (uint32_t)(g.tile * key_bytes);
   for (int c = 0; c < vals.n; ++c) {
     g.voff[c] = off;
@@ -641,29 +759,23 @@ ScatterGeom scatter_geom(cj_ctx* ctx, uint64_t n, int key_bytes, const ValCols& 
 void block_hist(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes, const PassPlan& plan,
                 const ScatterGeom& g, uint32_t* cnt_dev, uint32_t hparts) {
   const int np = plan.npasses;
-  uint32_t sh[8] = {}, mk[8] = {};
-  for (int p = 0; p < np && p < 8; ++p) {
-    sh[p] = plan.lo[p];
-    mk[p] = (1u << (plan.hi[p] - plan.lo[p])) - 1u;
+  if (np < 1 || np > 8) fail(CJ_ERR_UNSUPPORTED, "histogram of 1..8 passes");
+  HistArgs a{};
+  a.n = n;
+  a.tile = g.tile;
+  a.tiles = g.tiles;
+  a.nblocks = g.nblocks;
+  a.hparts = hparts;
+  for (int p = 0; p < np; ++p) {
+    a.shift[p] = plan.lo[p];
+    a.mask[p] = (1u << (plan.hi[p] - plan.lo[p])) - 1u;
   }
-  const uint4 s_lo{sh[0], sh[1], sh[2], sh[3]}, s_hi{sh[4], sh[5], sh[6], sh[7]};
-  const uint4 m_lo{mk[0], mk[1], mk[2], mk[3]}, m_hi{mk[4], mk[5], mk[6], mk[7]};
-  const size_t smem = sizeof(uint32_t) * kRadix * np * kHistWarps;
   CJ_CUDA(cudaMemsetAsync(cnt_dev, 0, sizeof(uint32_t) * kRadix * np * g.nblocks, ctx->stream));
   ctx->kbegin("histogram", n * key_bytes);
-  if (key_bytes == 4) {
-    CJ_CUDA(cudaFuncSetAttribute(k_block_hist<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-    k_block_hist<uint32_t><<<g.nblocks * kHistSub, kHistThreads, smem, ctx->stream>>>(
-        static_cast<const uint32_t*>(keys), n, g.tile, g.tiles, g.nblocks, np, s_lo, s_hi, m_lo,
-        m_hi, hparts, cnt_dev);
-  } else {
-    CJ_CUDA(cudaFuncSetAttribute(k_block_hist<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-    k_block_hist<uint64_t><<<g.nblocks * kHistSub, kHistThreads, smem, ctx->stream>>>(
-        static_cast<const uint64_t*>(keys), n, g.tile, g.tiles, g.nblocks, np, s_lo, s_hi, m_lo,
-        m_hi, hparts, cnt_dev);
-  }
+  if (key_bytes == 4)
+    launch_hist_np<uint32_t>(ctx, static_cast<const uint32_t*>(keys), a, np, cnt_dev);
+  else
+    launch_hist_np<uint64_t>(ctx, static_cast<const uint64_t*>(keys), a, np, cnt_dev);
   ctx->kend();
   CJ_CUDA(cudaGetLastError());
 }
@@ -725,13 +837,11 @@ void scatter_pass(cj_ctx* ctx, const void* keys_in, void* keys_out, uint64_t n, 
     }
     ctx->kbegin("scatter_pass", n * (row + wrow));
     if (key_bytes == 4) {
-      if (g.items == 8) launch_blocks<uint32_t, 8>(ctx, a, g.smem);
-      else if (g.items == 4) launch_blocks<uint32_t, 4>(ctx, a, g.smem);
-      else launch_blocks<uint32_t, 2>(ctx, a, g.smem);
+      if (g.rank == 1) launch_v2_items<uint32_t, 1>(ctx, a, g.smem, g.items);
+      else launch_v2_items<uint32_t, 0>(ctx, a, g.smem, g.items);
     } else {
-      if (g.items == 8) launch_blocks<uint64_t, 8>(ctx, a, g.smem);
-      else if (g.items == 4) launch_blocks<uint64_t, 4>(ctx, a, g.smem);
-      else launch_blocks<uint64_t, 2>(ctx, a, g.smem);
+      if (g.rank == 1) launch_v2_items<uint64_t, 1>(ctx, a, g.smem, g.items);
+      else launch_v2_items<uint64_t, 0>(ctx, a, g.smem, g.items);
     }
     ctx->kend();
     CJ_CUDA(cudaGetLastError());
@@ -787,8 +897,46 @@ void copy_columns(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, int
   }
 }
 
+namespace {
+void lsd_partition_group(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, int key_bytes,
+                         const PassPlan& plan, const ValCols& vals,
+                         std::vector<uint32_t>* counts_out);
+}  // namespace
+
+// Wide rows are partitioned in column groups of at most 32 payload bytes: each
+// group runs the same stable LSD plan with the key, so every group sees the same
+// permutation (the reference re-partitions each GFTR payload column with the key
+// the same way, join_engine.cpp:180-213).
 void lsd_partition(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, int key_bytes,
                    const PassPlan& plan, const ValCols& vals, std::vector<uint32_t>* counts_out) {
+  constexpr uint32_t kGroupBytes = 32;
+  uint32_t total = 0;
+  for (int c = 0; c < vals.n; ++c) total += vals.bytes[c];
+  if (total <= kGroupBytes) return lsd_partition_group(ctx, keys, keys_out, n, key_bytes, plan, vals,
+                                                       counts_out);
+  int c = 0;
+  bool first = true;
+  while (c < vals.n) {
+    ValCols g;
+    uint32_t bytes = 0;
+    while (c < vals.n && (g.n == 0 || bytes + vals.bytes[c] <= kGroupBytes)) {
+      g.in[g.n] = vals.in[c];
+      g.out[g.n] = vals.out[c];
+      g.bytes[g.n] = vals.bytes[c];
+      bytes += vals.bytes[c];
+      ++g.n;
+      ++c;
+    }
+    g.gen_ids = first ? vals.gen_ids : 0;
+    lsd_partition_group(ctx, keys, keys_out, n, key_bytes, plan, g, first ? counts_out : nullptr);
+    first = false;
+  }
+}
+
+namespace {
+void lsd_partition_group(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, int key_bytes,
+                         const PassPlan& plan, const ValCols& vals,
+                         std::vector<uint32_t>* counts_out) {
   if (plan.npasses > 8) fail(CJ_ERR_UNSUPPORTED, "LSD segment longer than 8 passes");
   const int np = plan.npasses;
   const ScatterGeom g0 = scatter_geom(ctx, n, key_bytes, vals, keys);
@@ -865,6 +1013,8 @@ void lsd_partition(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, in
   }
 }
 
+}  // namespace
+
 void shard_partition(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, int key_bytes,
                      uint32_t parts, const ValCols& vals, uint64_t* counts_host) {
   if (parts == 0 || parts > 256) fail(CJ_ERR_SPEC_INVALID, "shard count must be in [1, 256]");
@@ -903,3 +1053,13 @@ void partition_offsets(cj_ctx* ctx, const void* keys_sorted, uint64_t n, int key
 }
 
 }  // namespace cj
+
+#ifdef CJ_PHASE_CLOCKS
+extern "C" void cj_debug_phase_clocks(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, cj::g_phase_clk, sizeof(unsigned long long) * 16);
+  if (reset) {
+    unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(cj::g_phase_clk, z, sizeof(z));
+  }
+}
+#endif

@@ -708,7 +708,7 @@ JoinOutput run_join(const JoinTask& task) {
   if (task.options.radix_bits_per_pass == 0 || task.options.radix_bits_per_pass > 8)
     throw FanoutTooLarge("radix bits per pass must be in [1, 8]");
   if (r.payloads.size() > CJ_MAX_COLS || s.payloads.size() > CJ_MAX_COLS)
-    throw Unsupported("at most 8 payload columns per relation");
+    throw Unsupported("at most 16 payload columns per relation");
   auto& d = Device::get();
   std::lock_guard<std::mutex> lock(d.mu());
   std::vector<Buf> rc = upload_relation(r), sc = upload_relation(s);
