@@ -63,6 +63,10 @@ struct cj_ctx {
   uint16_t next_epoch();          // fresh look-back generation (memsets on wrap)
   uint64_t* status_buffer(uint64_t words);
   uint32_t* ticket(int slot);     // zeroed device counter (slot < 64)
+  // Grow the stream-ordered pool to hold `bytes` at once (one mapping), so a
+  // join's scratch never maps new memory mid-call (multi-ms stalls otherwise).
+  uint64_t pool_reserved = 0;
+  void reserve(uint64_t bytes);
 };
 
 namespace cj {

@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -264,6 +265,15 @@ void run_join_dev(cj_ctx* ctx, const cj_relation* R, const cj_relation* S,
   if (opt->algo == CJ_PHJ && (total_bits > 20 || total_bits > (unsigned)kb * 8))
     fail(CJ_ERR_FANOUT_TOO_LARGE, "partition fan-out capped at 2^20 and the key width");
   const bool want_ids = opt->want_ids || opt->want_stats;
+  {
+    // peak device footprint of the call: transformed R and S, one side's LSD
+    // ping-pong scratch, the output (|S| rows for PK-FK) and find scratch
+    uint64_t rb = R->key_bytes, sb = S->key_bytes, ob = R->key_bytes + 8;
+    for (uint32_t c = 0; c < R->npay; ++c) rb += R->pay_bytes[c], ob += R->pay_bytes[c];
+    for (uint32_t c = 0; c < S->npay; ++c) sb += S->pay_bytes[c], ob += S->pay_bytes[c];
+    const uint64_t big = std::max(rb * R->rows, sb * S->rows);
+    ctx->reserve(rb * R->rows + sb * S->rows + big + ob * S->rows + 4 * S->rows + (64ull << 20));
+  }
   std::memset(res, 0, sizeof(*res));
   std::vector<void*> owned;
   Timer tm(ctx);
@@ -504,6 +514,19 @@ uint16_t cj_ctx::next_epoch() {
   return ++epoch;
 }
 
+void cj_ctx::reserve(uint64_t bytes) {
+  if (bytes <= pool_reserved) return;
+  const uint64_t want = bytes + bytes / 4;
+  void* p = nullptr;
+  if (cudaMallocAsync(&p, want, stream) != cudaSuccess) {
+    cudaGetLastError();  // not enough memory for one block: allocate as we go
+    pool_reserved = bytes;
+    return;
+  }
+  cj::check_cuda(cudaFreeAsync(p, stream), "cudaFreeAsync");
+  pool_reserved = want;
+}
+
 uint64_t* cj_ctx::status_buffer(uint64_t words) {
   if (words > status_words) {
     if (status) cudaFreeAsync(status, stream);
@@ -575,6 +598,16 @@ int cj_ctx_create(int device, void* stream, cj_ctx** out) {
     CJ_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
     uint64_t thr = UINT64_MAX;
     CJ_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    // Optional up-front reservation (GiB) of the stream-ordered pool, so the
+    // join's multi-GiB scratch never maps new memory inside a timed call.
+    if (const char* rg = std::getenv("CJ_POOL_RESERVE_GB")) {
+      const uint64_t bytes = (uint64_t)std::strtoull(rg, nullptr, 10) << 30;
+      if (bytes) {
+        void* p = nullptr;
+        CJ_CUDA(cudaMallocAsync(&p, bytes, ctx->stream));
+        CJ_CUDA(cudaFreeAsync(p, ctx->stream));
+      }
+    }
     ctx->counters = static_cast<uint32_t*>(ctx->alloc(256 * sizeof(uint32_t)));
     CJ_CUDA(cudaMemsetAsync(ctx->counters, 0, 256 * sizeof(uint32_t), ctx->stream));
     ctx->err_word = ctx->counters + 128;

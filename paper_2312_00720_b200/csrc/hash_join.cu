@@ -153,6 +153,12 @@ struct FindArgs {
   uint64_t* unit_off;        // exclusive output offset per unit (fill)
   uint64_t nb_rows, np_rows; // sizes of the partitioned inputs
   int stages;                // 2: prefetch the next unit while this one runs
+  // count pass -> fill pass hand-off: build-chunk index of every probe row's
+  // match (0xffff: none) and a per-unit duplicate flag; fill units without
+  // duplicates then skip the table build and the probe entirely
+  uint16_t* match_e;
+  uint8_t* unit_dup;
+  uint32_t off_e;            // stage offset of the match_e chunk
 };
 
 template <class K>
@@ -422,12 +428,96 @@ __global__ void k_phj_desc(const uint64_t* __restrict__ boff, const uint64_t* __
   }
 }
 
+// GFTR/GFUR emission of a unit without duplicate build keys: compact the hits
+// in probe order (list[t] = build idx << 16 | probe idx), then write column by
+// column, consecutive threads on consecutive output rows.  The match of probe
+// row jl is me[jl] (0xffff: none) when the count pass resolved it, else res[jl].
+template <class K>
+__device__ __forceinline__ void emit_compact(const FindArgs& a, const UnitDesc& inf,
+                                             const uint8_t* st, const K* pk, const uint16_t* me,
+                                             const uint32_t* res, uint32_t r0, uint32_t r1,
+                                             uint32_t nq, const uint64_t* s_wbase,
+                                             const uint64_t* s_wcount, uint32_t* list) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t bsh4 = (uint32_t)(inf.b_lo & 3), bsh8 = (uint32_t)(inf.b_lo & 1);
+  const uint32_t qsh4 = (uint32_t)(inf.q_lo & 3), qsh8 = (uint32_t)(inf.q_lo & 1);
+    // 3a. compact the hits in probe order: list[t] = (build idx << 16) | probe idx
+    const uint64_t ubase = s_wbase[0];
+    uint32_t o = (uint32_t)(s_wbase[warp] - ubase);
+    for (uint32_t r = r0; r < r1; ++r) {
+      const uint32_t jl = r * 32 + lane;
+      uint32_t e = kNoMatch;
+      if (jl < nq) e = me ? (me[jl] == kEmpty16 ? kNoMatch : (uint32_t)me[jl]) : res[jl];
+      const bool hit = e != kNoMatch;
+      const uint32_t bal = __ballot_sync(0xffffffffu, hit);
+      if (hit) list[o + __popc(bal & dev::lanemask_lt())] = (e << 16) | jl;
+      o += __popc(bal);
+    }
+    __syncthreads();
+    // 3b. column by column, consecutive threads write consecutive output rows
+    uint32_t cnt = (uint32_t)(s_wbase[kTmaWarps - 1] - ubase + s_wcount[kTmaWarps - 1]);
+    if (ubase + cnt > a.capacity) cnt = ubase < a.capacity ? (uint32_t)(a.capacity - ubase) : 0u;
+    constexpr int kE = 8;
+    for (uint32_t t0 = 0; t0 < cnt; t0 += kE * kTmaThreads) {
+      uint32_t L[kE];
+#pragma unroll
+      for (int k = 0; k < kE; ++k) {
+        const uint32_t t = t0 + tid + k * kTmaThreads;
+        L[k] = t < cnt ? list[t] : 0u;
+      }
+      auto each = [&](auto&& f) {
+#pragma unroll
+        for (int k = 0; k < kE; ++k) {
+          const uint32_t t = t0 + tid + k * kTmaThreads;
+          if (t < cnt) f(ubase + t, L[k] >> 16, L[k] & 0xffffu);
+        }
+      };
+      if (a.key_out) {
+        K* ko = static_cast<K*>(a.key_out);
+        each([&](uint64_t oo, uint32_t, uint32_t jl) { ko[oo] = pk[jl]; });
+      }
+      if (a.ids_r)
+        each([&](uint64_t oo, uint32_t li, uint32_t) {
+          const uint64_t gi = inf.b_lo + li;
+          a.ids_r[oo] = a.carried_r ? a.carried_r[gi] : (uint32_t)gi;
+        });
+      if (a.ids_s)
+        each([&](uint64_t oo, uint32_t, uint32_t jl) {
+          const uint64_t j = inf.q_lo + jl;
+          a.ids_s[oo] = a.carried_s ? a.carried_s[j] : (uint32_t)j;
+        });
+      for (int c = 0; c < a.nr; ++c) {
+        if (a.r_bytes[c] == 4) {
+          const uint32_t* sv = reinterpret_cast<const uint32_t*>(st + a.off_r[c]) + bsh4;
+          uint32_t* dv = static_cast<uint32_t*>(a.r_dst[c]);
+          each([&](uint64_t oo, uint32_t li, uint32_t) { dv[oo] = sv[li]; });
+        } else {
+          const uint64_t* sv = reinterpret_cast<const uint64_t*>(st + a.off_r[c]) + bsh8;
+          uint64_t* dv = static_cast<uint64_t*>(a.r_dst[c]);
+          each([&](uint64_t oo, uint32_t li, uint32_t) { dv[oo] = sv[li]; });
+        }
+      }
+      for (int c = 0; c < a.ns; ++c) {
+        if (a.s_bytes[c] == 4) {
+          const uint32_t* sv = reinterpret_cast<const uint32_t*>(st + a.off_s[c]) + qsh4;
+          uint32_t* dv = static_cast<uint32_t*>(a.s_dst[c]);
+          each([&](uint64_t oo, uint32_t, uint32_t jl) { dv[oo] = sv[jl]; });
+        } else {
+          const uint64_t* sv = reinterpret_cast<const uint64_t*>(st + a.off_s[c]) + qsh8;
+          uint64_t* dv = static_cast<uint64_t*>(a.s_dst[c]);
+          each([&](uint64_t oo, uint32_t, uint32_t jl) { dv[oo] = sv[jl]; });
+        }
+      }
+    }
+}
+
 template <class K, bool WRITE>
 __global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constant__ FindArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint32_t* tab = reinterpret_cast<uint32_t*>(smem + (size_t)a.stages * a.stage_bytes);
   uint32_t* res = tab + a.cap_entries;
   __shared__ UnitDesc s_desc[2];
+  __shared__ bool s_pre[2];
   __shared__ __align__(8) uint64_t mbar[2];
   __shared__ uint64_t s_wcount[kTmaWarps], s_wbase[kTmaWarps];
   __shared__ int s_dup;
@@ -440,37 +530,47 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constan
   auto bytes = [&](uint64_t lo, uint64_t hi, uint32_t w) {
     return (uint32_t)((dev::align_hi(hi, w) - dev::align_lo(lo, w)) * w);
   };
-  auto issue = [&](int b, const UnitDesc& d) {  // thread 0
+  // pre: the count pass resolved this unit's matches (match_e); no build keys needed
+  auto issue = [&](int b, const UnitDesc& d, bool pre) {  // thread 0
     uint8_t* st = smem + (size_t)b * a.stage_bytes;
-    uint32_t total = bytes(d.b_lo, d.b_hi, kb) + bytes(d.q_lo, d.q_hi, kb);
+    uint32_t total = bytes(d.q_lo, d.q_hi, kb);
+    if (!pre) total += bytes(d.b_lo, d.b_hi, kb);
     if (WRITE) {
       for (int c = 0; c < a.nr; ++c) total += bytes(d.b_lo, d.b_hi, a.r_bytes[c]);
       for (int c = 0; c < a.ns; ++c) total += bytes(d.q_lo, d.q_hi, a.s_bytes[c]);
+      if (pre) total += bytes(d.q_lo, d.q_hi, 2);
     }
     dev::mbar_expect_tx(&mbar[b], total);
     auto copy = [&](uint32_t off, const void* base, uint64_t lo, uint64_t hi, uint32_t w) {
       dev::tma_load_1d(st + off, static_cast<const uint8_t*>(base) + dev::align_lo(lo, w) * w,
                        bytes(lo, hi, w), &mbar[b]);
     };
-    copy(a.off_bk, a.bkeys, d.b_lo, d.b_hi, kb);
+    if (!pre) copy(a.off_bk, a.bkeys, d.b_lo, d.b_hi, kb);
     copy(a.off_pk, a.pkeys, d.q_lo, d.q_hi, kb);
     if (WRITE) {
       for (int c = 0; c < a.nr; ++c) copy(a.off_r[c], a.r_src[c], d.b_lo, d.b_hi, a.r_bytes[c]);
       for (int c = 0; c < a.ns; ++c) copy(a.off_s[c], a.s_src[c], d.q_lo, d.q_hi, a.s_bytes[c]);
+      if (pre) copy(a.off_e, a.match_e, d.q_lo, d.q_hi, 2);
     }
   };
+  auto is_pre = [&](uint64_t uu) { return WRITE && a.match_e != nullptr && a.unit_dup[uu] == 0; };
 
   uint64_t u = blockIdx.x;
   UnitDesc next{};  // descriptor of the unit after the one in flight (thread 0)
+  bool next_pre = false;
   if (tid == 0) {
     dev::mbar_init(&mbar[0], 1);
     dev::mbar_init(&mbar[1], 1);
     dev::fence_mbar_init();
     if (u < units) {
       s_desc[0] = descs[u];
-      issue(0, s_desc[0]);
+      s_pre[0] = is_pre(u);
+      issue(0, s_desc[0], s_pre[0]);
     }
-    if (u + gridDim.x < units) next = descs[u + gridDim.x];
+    if (u + gridDim.x < units) {
+      next = descs[u + gridDim.x];
+      next_pre = is_pre(u + gridDim.x);
+    }
   }
   __syncthreads();
   uint32_t phase[2] = {0, 0};
@@ -478,13 +578,18 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constan
   auto issue_next = [&](int nb_) {  // thread 0: copies of unit u + gridDim.x into stage nb_
     if (u + gridDim.x < units) {
       s_desc[nb_] = next;
+      s_pre[nb_] = next_pre;
       dev::fence_proxy_async();
-      issue(nb_, next);
-      if (u + 2ull * gridDim.x < units) next = descs[u + 2ull * gridDim.x];  // in flight
+      issue(nb_, next, next_pre);
+      if (u + 2ull * gridDim.x < units) {  // in flight
+        next = descs[u + 2ull * gridDim.x];
+        next_pre = is_pre(u + 2ull * gridDim.x);
+      }
     }
   };
   for (; u < units; u += gridDim.x, b = (b + 1) % a.stages) {
     const UnitDesc inf = s_desc[b];
+    const bool pre = s_pre[b];
     if (tid == 0) {
       if (a.stages == 2) issue_next(b ^ 1);
       s_dup = 0;
@@ -492,13 +597,43 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constan
     uint64_t unit_base = 0;
     if (WRITE && tid == 32 && a.unit_off) unit_base = a.unit_off[u];
     const uint32_t nb = (uint32_t)(inf.b_hi - inf.b_lo), nq = (uint32_t)(inf.q_hi - inf.q_lo);
+    uint8_t* st = smem + (size_t)b * a.stage_bytes;
+    const K* bk = reinterpret_cast<const K*>(st + a.off_bk) + (inf.b_lo - dev::align_lo(inf.b_lo, kb));
+    const K* pk = reinterpret_cast<const K*>(st + a.off_pk) + (inf.q_lo - dev::align_lo(inf.q_lo, kb));
+    const uint32_t rounds = (nq + 31) / 32;
+    const uint32_t r0 = (uint32_t)((uint64_t)rounds * warp / kTmaWarps);
+    const uint32_t r1 = (uint32_t)((uint64_t)rounds * (warp + 1) / kTmaWarps);
+    if (pre) {
+      // matches resolved by the count pass: count this warp's hits, then
+      // continue at the compaction below (res <- match_e)
+      const uint16_t* me = reinterpret_cast<const uint16_t*>(st + a.off_e) +
+                           (inf.q_lo - dev::align_lo(inf.q_lo, 2));
+      dev::mbar_wait(&mbar[b], phase[b]);
+      phase[b] ^= 1;
+      uint64_t wc = 0;
+      for (uint32_t r = r0; r < r1; ++r) {
+        const uint32_t jl = r * 32 + lane;
+        const bool hit = jl < nq && me[jl] != kEmpty16;
+        wc += __popc(__ballot_sync(0xffffffffu, hit));
+      }
+      if (lane == 0) s_wcount[warp] = wc;
+      __syncthreads();
+      if (warp == 1) {
+        const uint64_t c = lane < kTmaWarps ? s_wcount[lane] : 0;
+        const uint64_t inc = dev::warp_inclusive_sum(c);
+        const uint64_t base = __shfl_sync(0xffffffffu, unit_base, 0);
+        if (lane < kTmaWarps) s_wbase[lane] = base + inc - c;
+      }
+      __syncthreads();
+      emit_compact<K>(a, inf, st, pk, me, nullptr, r0, r1, nq, s_wbase, s_wcount, res + a.qchunk);
+      __syncthreads();
+      if (a.stages == 1 && tid == 0) issue_next(0);
+      continue;
+    }
     uint32_t cap_log2 = 1;
     while ((1u << cap_log2) < 2 * nb) ++cap_log2;
     const uint32_t cap = 1u << cap_log2, cmask = cap - 1;
     for (uint32_t i = tid; i < cap; i += kTmaThreads) tab[i] = kNoMatch;
-    uint8_t* st = smem + (size_t)b * a.stage_bytes;
-    const K* bk = reinterpret_cast<const K*>(st + a.off_bk) + (inf.b_lo - dev::align_lo(inf.b_lo, kb));
-    const K* pk = reinterpret_cast<const K*>(st + a.off_pk) + (inf.q_lo - dev::align_lo(inf.q_lo, kb));
     dev::mbar_wait(&mbar[b], phase[b]);
     phase[b] ^= 1;
     __syncthreads();
@@ -518,6 +653,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constan
     if (__syncthreads_or(dup)) s_dup = 1;
     __syncthreads();
     const bool has_dup = s_dup != 0;
+    if (!WRITE && a.unit_dup && tid == 0) a.unit_dup[u] = has_dup ? 1 : 0;
     uint16_t* sidx = reinterpret_cast<uint16_t*>(tab);
     if (has_dup) {  // stably sorted chunk positions: bitonic over (key, position)
       uint32_t np2 = 1;
@@ -543,9 +679,6 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constan
     }
 
     // 2. probe from shared memory; warp w owns a contiguous run of rounds
-    const uint32_t rounds = (nq + 31) / 32;
-    const uint32_t r0 = (uint32_t)((uint64_t)rounds * warp / kTmaWarps);
-    const uint32_t r1 = (uint32_t)((uint64_t)rounds * (warp + 1) / kTmaWarps);
     uint64_t wcount = 0;
     for (uint32_t r = r0; r < r1; ++r) {
       const uint32_t jl = r * 32 + lane;
@@ -575,6 +708,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constan
           out = (lo << 16) | m;
         }
         if (WRITE) res[jl] = out;
+        else if (a.match_e && !has_dup)
+          a.match_e[inf.q_lo + jl] = (uint16_t)(out == kNoMatch ? kEmpty16 : out);
         wcount += m;
       }
     }
@@ -629,74 +764,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constan
       }
     };
     if (!has_dup) {
-      // 3a. compact the hits in probe order: list[t] = (build idx << 16) | probe idx
-      uint32_t* list = res + a.qchunk;
-      const uint64_t ubase = s_wbase[0];
-      uint32_t o = (uint32_t)(s_wbase[warp] - ubase);
-      for (uint32_t r = r0; r < r1; ++r) {
-        const uint32_t jl = r * 32 + lane;
-        const uint32_t e = jl < nq ? res[jl] : kNoMatch;
-        const bool hit = e != kNoMatch;
-        const uint32_t bal = __ballot_sync(0xffffffffu, hit);
-        if (hit) list[o + __popc(bal & dev::lanemask_lt())] = (e << 16) | jl;
-        o += __popc(bal);
-      }
-      __syncthreads();
-      // 3b. column by column, consecutive threads write consecutive output rows
-      uint32_t cnt = (uint32_t)(s_wbase[kTmaWarps - 1] - ubase + s_wcount[kTmaWarps - 1]);
-      if (ubase + cnt > a.capacity) cnt = ubase < a.capacity ? (uint32_t)(a.capacity - ubase) : 0u;
-      constexpr int kE = 8;
-      for (uint32_t t0 = 0; t0 < cnt; t0 += kE * kTmaThreads) {
-        uint32_t L[kE];
-#pragma unroll
-        for (int k = 0; k < kE; ++k) {
-          const uint32_t t = t0 + tid + k * kTmaThreads;
-          L[k] = t < cnt ? list[t] : 0u;
-        }
-        auto each = [&](auto&& f) {
-#pragma unroll
-          for (int k = 0; k < kE; ++k) {
-            const uint32_t t = t0 + tid + k * kTmaThreads;
-            if (t < cnt) f(ubase + t, L[k] >> 16, L[k] & 0xffffu);
-          }
-        };
-        if (a.key_out) {
-          K* ko = static_cast<K*>(a.key_out);
-          each([&](uint64_t oo, uint32_t, uint32_t jl) { ko[oo] = pk[jl]; });
-        }
-        if (a.ids_r)
-          each([&](uint64_t oo, uint32_t li, uint32_t) {
-            const uint64_t gi = inf.b_lo + li;
-            a.ids_r[oo] = a.carried_r ? a.carried_r[gi] : (uint32_t)gi;
-          });
-        if (a.ids_s)
-          each([&](uint64_t oo, uint32_t, uint32_t jl) {
-            const uint64_t j = inf.q_lo + jl;
-            a.ids_s[oo] = a.carried_s ? a.carried_s[j] : (uint32_t)j;
-          });
-        for (int c = 0; c < a.nr; ++c) {
-          if (a.r_bytes[c] == 4) {
-            const uint32_t* sv = reinterpret_cast<const uint32_t*>(st + a.off_r[c]) + bsh4;
-            uint32_t* dv = static_cast<uint32_t*>(a.r_dst[c]);
-            each([&](uint64_t oo, uint32_t li, uint32_t) { dv[oo] = sv[li]; });
-          } else {
-            const uint64_t* sv = reinterpret_cast<const uint64_t*>(st + a.off_r[c]) + bsh8;
-            uint64_t* dv = static_cast<uint64_t*>(a.r_dst[c]);
-            each([&](uint64_t oo, uint32_t li, uint32_t) { dv[oo] = sv[li]; });
-          }
-        }
-        for (int c = 0; c < a.ns; ++c) {
-          if (a.s_bytes[c] == 4) {
-            const uint32_t* sv = reinterpret_cast<const uint32_t*>(st + a.off_s[c]) + qsh4;
-            uint32_t* dv = static_cast<uint32_t*>(a.s_dst[c]);
-            each([&](uint64_t oo, uint32_t, uint32_t jl) { dv[oo] = sv[jl]; });
-          } else {
-            const uint64_t* sv = reinterpret_cast<const uint64_t*>(st + a.off_s[c]) + qsh8;
-            uint64_t* dv = static_cast<uint64_t*>(a.s_dst[c]);
-            each([&](uint64_t oo, uint32_t, uint32_t jl) { dv[oo] = sv[jl]; });
-          }
-        }
-      }
+      emit_compact<K>(a, inf, st, pk, nullptr, res, r0, r1, nq, s_wbase, s_wcount, res + a.qchunk);
       __syncthreads();
       if (a.stages == 1 && tid == 0) issue_next(0);
       continue;
@@ -776,6 +844,10 @@ bool tma_layout(FindArgs& a, size_t* smem_out) {
     a.off_s[c] = (uint32_t)off;
     off = up(off + (size_t)(a.qchunk + 8) * a.s_bytes[c]);
   }
+  if (a.write && a.match_e) {
+    a.off_e = (uint32_t)off;
+    off = up(off + (size_t)(a.qchunk + 8) * 2);
+  }
   a.stage_bytes = (uint32_t)off;
   a.cap_entries = 1u << a.cap_log2;
   // + res[qchunk] probe results + list[qchunk] compacted hits
@@ -799,6 +871,15 @@ uint64_t run_find(cj_ctx* ctx, FindArgs a, uint64_t total_units) {
   size_t tma_smem = 0;
   const char* mode = std::getenv("CJ_FIND");
   const bool want_tma = !(mode && std::strcmp(mode, "ldg") == 0);
+  // count pass -> fill pass hand-off (see FindArgs::match_e)
+  const char* me_env = std::getenv("CJ_FIND_HANDOFF");
+  const bool handoff = a.write && a.padded && a.desc && !(me_env && std::strcmp(me_env, "0") == 0);
+  Scratch me_buf(ctx, handoff ? a.np_rows * 2 + kPad : 0);
+  Scratch dup_buf(ctx, handoff ? total_units + 16 : 0);
+  if (handoff) {
+    a.match_e = me_buf.as<uint16_t>();
+    a.unit_dup = dup_buf.as<uint8_t>();
+  }
   if (want_tma && a.padded && a.desc && tma_layout<K>(a, &tma_smem)) {
     // count pass (keys only) -> scan -> fill pass; no inter-CTA waiting
     const uint64_t U = total_units;
@@ -809,6 +890,8 @@ uint64_t run_find(cj_ctx* ctx, FindArgs a, uint64_t total_units) {
       const unsigned grid =
           (unsigned)std::min<uint64_t>((uint64_t)ctx->num_sms * find_ctas_per_sm(), U);
       a.unit_off = nullptr;
+      a.match_e = nullptr;
+      a.unit_dup = nullptr;
       CJ_CUDA(cudaFuncSetAttribute(k_phj_tma<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)tma_smem));
       ctx->kbegin("phj_find", 0);
@@ -826,6 +909,7 @@ uint64_t run_find(cj_ctx* ctx, FindArgs a, uint64_t total_units) {
       Scratch counts(ctx, U * 8), offs(ctx, U * 8);
       FindArgs ac = a;
       ac.nr = ac.ns = 0;
+      ac.write = 0;
       ac.unit_counts = counts.as<uint64_t>();
       size_t smem_c = 0;
       tma_layout<K>(ac, &smem_c);

@@ -66,6 +66,10 @@ struct SmjArgs {
   uint64_t* tile_off;
   uint32_t stage_bytes, off_rk, off_sk, off_r[CJ_MAX_COLS], off_s[CJ_MAX_COLS];
   int padded;
+  // count -> fill hand-off for PK-FK tiles (see k_smj_tma)
+  uint16_t* match_e;
+  uint8_t* tile_pre;
+  uint32_t off_e;
 };
 
 template <class K>
@@ -246,12 +250,43 @@ __global__ void k_smj_bounds(const K* __restrict__ r, uint64_t nr, const K* __re
   }
 }
 
+// Galloping lower/upper bound in a shared-memory run starting at `from`
+// (monotone probes: the next probe's bound is at or after the previous one).
+template <class K, bool UPPER>
+__device__ __forceinline__ uint32_t gallop(const K* __restrict__ r, uint32_t from, uint32_t n, K k) {
+  auto before = [&](uint32_t i) { return UPPER ? !(k < r[i]) : r[i] < k; };
+  if (from >= n || !before(from)) return from;
+  uint32_t lo = from + 1, step = 1;  // r[lo - 1] is before k
+  while (lo + step <= n && before(lo + step - 1)) {
+    lo += step;
+    step <<= 1;
+  }
+  uint32_t hi = min(n, lo + step - 1);
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (before(mid)) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// Persistent CTAs take tiles of kTileS probe positions; each thread owns four
+// consecutive probes (one binary search, then galloping), so a warp owns 128
+// consecutive probes and emission keeps probe order.  WRITE=false: per-tile
+// match counts and, for PK-FK tiles whose r window fits shared memory, the
+// window index of every probe's match (match_e, 0xffff: none) so the fill pass
+// skips the search and the r keys.  WRITE=true: compact the hits of the tile
+// (list[t] = window idx << 16 | probe idx) and write column by column.
+constexpr uint32_t kSmjPer = kTileS / kTmaThreads;  // probes per thread (4)
+constexpr uint32_t kSmjList = 2 * kTileS;            // compacted rows per tile in shared memory
+
 template <class K, bool WRITE>
 __global__ void __launch_bounds__(kTmaThreads, 1) k_smj_tma(const __grid_constant__ SmjArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint32_t* loff = reinterpret_cast<uint32_t*>(smem + 2 * (size_t)a.stage_bytes);
   uint32_t* mcnt = loff + kTileS;
+  uint32_t* list = mcnt + kTileS;  // [kSmjList] (WRITE)
   __shared__ SmjDesc s_desc[2];
+  __shared__ bool s_pre[2];
   __shared__ __align__(8) uint64_t mbar[2];
   __shared__ uint64_t s_wcount[kTmaWarps], s_wbase[kTmaWarps];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -261,15 +296,17 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_smj_tma(const __grid_constan
   auto bytes = [&](uint64_t lo, uint64_t hi, uint32_t w) {
     return hi > lo ? (uint32_t)((dev::align_hi(hi, w) - dev::align_lo(lo, w)) * w) : 0u;
   };
-  auto issue = [&](int b, const SmjDesc& d) {  // thread 0
+  auto is_pre = [&](uint64_t tt) { return WRITE && a.match_e != nullptr && a.tile_pre[tt] != 0; };
+  auto issue = [&](int b, const SmjDesc& d, bool pre) {  // thread 0
     uint8_t* st = smem + (size_t)b * a.stage_bytes;
     const bool win = d.r_hi - d.r_lo <= a.wmax;
     uint32_t total = bytes(d.s_lo, d.s_hi, kb);
-    if (win) total += bytes(d.r_lo, d.r_hi, kb);
+    if (win && !pre) total += bytes(d.r_lo, d.r_hi, kb);
     if (WRITE) {
       if (win)
         for (int c = 0; c < a.nr_cols; ++c) total += bytes(d.r_lo, d.r_hi, a.r_bytes[c]);
       for (int c = 0; c < a.ns_cols; ++c) total += bytes(d.s_lo, d.s_hi, a.s_bytes[c]);
+      if (pre) total += bytes(d.s_lo, d.s_hi, 2);
     }
     dev::mbar_expect_tx(&mbar[b], total);
     auto copy = [&](uint32_t off, const void* base, uint64_t lo, uint64_t hi, uint32_t w) {
@@ -278,35 +315,46 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_smj_tma(const __grid_constan
                          bytes(lo, hi, w), &mbar[b]);
     };
     copy(a.off_sk, a.s, d.s_lo, d.s_hi, kb);
-    if (win) copy(a.off_rk, a.r, d.r_lo, d.r_hi, kb);
+    if (win && !pre) copy(a.off_rk, a.r, d.r_lo, d.r_hi, kb);
     if (WRITE) {
       if (win)
         for (int c = 0; c < a.nr_cols; ++c) copy(a.off_r[c], a.r_src[c], d.r_lo, d.r_hi, a.r_bytes[c]);
       for (int c = 0; c < a.ns_cols; ++c) copy(a.off_s[c], a.s_src[c], d.s_lo, d.s_hi, a.s_bytes[c]);
+      if (pre) copy(a.off_e, a.match_e, d.s_lo, d.s_hi, 2);
     }
   };
   uint64_t t = blockIdx.x;
   SmjDesc next{};
+  bool next_pre = false;
   if (tid == 0) {
     dev::mbar_init(&mbar[0], 1);
     dev::mbar_init(&mbar[1], 1);
     dev::fence_mbar_init();
     if (t < a.tiles) {
       s_desc[0] = descs[t];
-      issue(0, s_desc[0]);
+      s_pre[0] = is_pre(t);
+      issue(0, s_desc[0], s_pre[0]);
     }
-    if (t + gridDim.x < a.tiles) next = descs[t + gridDim.x];
+    if (t + gridDim.x < a.tiles) {
+      next = descs[t + gridDim.x];
+      next_pre = is_pre(t + gridDim.x);
+    }
   }
   __syncthreads();
   uint32_t phase[2] = {0, 0};
   int b = 0;
   for (; t < a.tiles; t += gridDim.x, b ^= 1) {
     const SmjDesc d = s_desc[b];
+    const bool pre = s_pre[b];
     if (tid == 0 && t + gridDim.x < a.tiles) {
       s_desc[b ^ 1] = next;
+      s_pre[b ^ 1] = next_pre;
       dev::fence_proxy_async();
-      issue(b ^ 1, next);
-      if (t + 2ull * gridDim.x < a.tiles) next = descs[t + 2ull * gridDim.x];
+      issue(b ^ 1, next, next_pre);
+      if (t + 2ull * gridDim.x < a.tiles) {
+        next = descs[t + 2ull * gridDim.x];
+        next_pre = is_pre(t + 2ull * gridDim.x);
+      }
     }
     uint64_t tile_base = 0;
     if (WRITE && tid == 32) tile_base = a.tile_off[t];
@@ -320,46 +368,63 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_smj_tma(const __grid_constan
     phase[b] ^= 1;
     __syncthreads();
 
-    const uint32_t rounds = (nq + 31) / 32;
-    const uint32_t r0 = rounds * warp / kTmaWarps, r1 = rounds * (warp + 1) / kTmaWarps;
-    uint64_t wc = 0;
-    for (uint32_t rr = r0; rr < r1; ++rr) {
-      const uint32_t jl = rr * 32 + lane;
-      if (jl >= nq) continue;
-      const K k = sk[jl];
-      uint64_t lb, m = 0;
-      if (win) {
-        uint32_t lo = 0, hi = (uint32_t)w;
-        while (lo < hi) {
-          const uint32_t mid = (lo + hi) >> 1;
-          if (rk[mid] < k) lo = mid + 1; else hi = mid;
-        }
-        lb = lo;
-        if (lo < w && rk[lo] == k) {
-          if (a.pk_fk) {
-            m = 1;
-          } else {
-            uint32_t lo2 = lo + 1, hi2 = (uint32_t)w;
-            while (lo2 < hi2) {
-              const uint32_t mid = (lo2 + hi2) >> 1;
-              if (rk[mid] <= k) lo2 = mid + 1; else hi2 = mid;
+    // 1. bounds of this thread's four probes
+    const uint32_t j0 = tid * kSmjPer;
+    uint32_t tsum = 0;
+    if (pre) {
+      const uint16_t* me = reinterpret_cast<const uint16_t*>(st + a.off_e) +
+                           (d.s_lo - dev::align_lo(d.s_lo, 2));
+#pragma unroll
+      for (uint32_t q = 0; q < kSmjPer; ++q) {
+        const uint32_t jl = j0 + q;
+        const uint32_t e = jl < nq ? me[jl] : 0xffffu;
+        loff[jl] = e;
+        mcnt[jl] = e != 0xffffu;
+        tsum += e != 0xffffu;
+      }
+    } else if (win) {
+      uint32_t lb = 0;
+#pragma unroll
+      for (uint32_t q = 0; q < kSmjPer; ++q) {
+        const uint32_t jl = j0 + q;
+        if (jl < nq) {
+          const K k = sk[jl];
+          if (q == 0) {
+            uint32_t lo = 0, hi = (uint32_t)w;
+            while (lo < hi) {
+              const uint32_t mid = (lo + hi) >> 1;
+              if (rk[mid] < k) lo = mid + 1; else hi = mid;
             }
-            m = lo2 - lo;
+            lb = lo;
+          } else {
+            lb = gallop<K, false>(rk, lb, (uint32_t)w, k);
           }
+          uint32_t m = 0;
+          if (lb < w && rk[lb] == k) m = a.pk_fk ? 1u : gallop<K, true>(rk, lb, (uint32_t)w, k) - lb;
+          loff[jl] = lb;
+          mcnt[jl] = m;
+          tsum += m;
+          if (!WRITE && a.match_e) a.match_e[d.s_lo + jl] = (uint16_t)(m ? lb : 0xffffu);
         }
-      } else {
-        const uint64_t g = g_lower_bound<K>(rg, d.r_lo, d.r_hi, k);
-        lb = g - d.r_lo;
-        if (g < d.r_hi && rg[g] == k) m = a.pk_fk ? 1 : g_upper_bound<K>(rg, g, d.r_hi, k) - g;
       }
-      if (WRITE) {
-        loff[jl] = (uint32_t)lb;
-        mcnt[jl] = (uint32_t)m;
+    } else {  // window beyond shared memory: global binary searches
+#pragma unroll
+      for (uint32_t q = 0; q < kSmjPer; ++q) {
+        const uint32_t jl = j0 + q;
+        if (jl < nq) {
+          const K k = sk[jl];
+          const uint64_t g = g_lower_bound<K>(rg, d.r_lo, d.r_hi, k);
+          uint64_t m = 0;
+          if (g < d.r_hi && rg[g] == k) m = a.pk_fk ? 1 : g_upper_bound<K>(rg, g, d.r_hi, k) - g;
+          loff[jl] = (uint32_t)(g - d.r_lo);
+          mcnt[jl] = (uint32_t)m;
+          tsum += (uint32_t)m;
+        }
       }
-      wc += m;
     }
-    wc = dev::warp_sum(wc);
-    if (lane == 0) s_wcount[warp] = wc;
+    if (!WRITE && a.match_e && tid == 0) a.tile_pre[t] = (a.pk_fk && win) ? 1 : 0;
+    const uint32_t tinc = dev::warp_inclusive_sum(tsum);
+    if (lane == 31) s_wcount[warp] = tinc;
     __syncthreads();
     if (warp == 1) {
       const uint64_t v = lane < kTmaWarps ? s_wcount[lane] : 0;
@@ -372,6 +437,78 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_smj_tma(const __grid_constan
     __syncthreads();
     const uint32_t ssh4 = (uint32_t)(d.s_lo & 3), ssh8 = (uint32_t)(d.s_lo & 1);
     const uint32_t rsh4 = (uint32_t)(d.r_lo & 3), rsh8 = (uint32_t)(d.r_lo & 1);
+    const uint64_t tbase = s_wbase[0];
+    const uint64_t tcount = s_wbase[kTmaWarps - 1] + s_wcount[kTmaWarps - 1] - tbase;
+    if (win && tcount <= kSmjList) {
+      // 2a. compact in (probe, r) order
+      uint32_t o = (uint32_t)(s_wbase[warp] - tbase) + tinc - tsum;
+      for (uint32_t q = 0; q < kSmjPer; ++q) {
+        const uint32_t jl = j0 + q;
+        if (jl < nq) {
+          const uint32_t m = mcnt[jl], l0 = loff[jl];
+          for (uint32_t i = 0; i < m; ++i) list[o++] = ((l0 + i) << 16) | jl;
+        }
+      }
+      __syncthreads();
+      // 2b. column by column, consecutive threads on consecutive output rows
+      uint32_t cnt = (uint32_t)tcount;
+      if (tbase + cnt > a.capacity) cnt = tbase < a.capacity ? (uint32_t)(a.capacity - tbase) : 0u;
+      constexpr int kE = kSmjList / kTmaThreads;
+      uint32_t L[kE];
+#pragma unroll
+      for (int k = 0; k < kE; ++k) {
+        const uint32_t tt = tid + k * kTmaThreads;
+        L[k] = tt < cnt ? list[tt] : 0u;
+      }
+      auto each = [&](auto&& f) {
+#pragma unroll
+        for (int k = 0; k < kE; ++k) {
+          const uint32_t tt = tid + k * kTmaThreads;
+          if (tt < cnt) f(tbase + tt, L[k] >> 16, L[k] & 0xffffu);
+        }
+      };
+      if (a.key_out) {
+        K* ko = static_cast<K*>(a.key_out);
+        each([&](uint64_t oo, uint32_t, uint32_t jl) { ko[oo] = sk[jl]; });
+      }
+      if (a.ids_r)
+        each([&](uint64_t oo, uint32_t li, uint32_t) {
+          const uint64_t i = d.r_lo + li;
+          a.ids_r[oo] = a.carried_r ? a.carried_r[i] : (uint32_t)i;
+        });
+      if (a.ids_s)
+        each([&](uint64_t oo, uint32_t, uint32_t jl) {
+          const uint64_t j = d.s_lo + jl;
+          a.ids_s[oo] = a.carried_s ? a.carried_s[j] : (uint32_t)j;
+        });
+      for (int c = 0; c < a.nr_cols; ++c) {
+        if (a.r_bytes[c] == 4) {
+          const uint32_t* sv = reinterpret_cast<const uint32_t*>(st + a.off_r[c]) + rsh4;
+          uint32_t* dv = static_cast<uint32_t*>(a.r_dst[c]);
+          each([&](uint64_t oo, uint32_t li, uint32_t) { dv[oo] = sv[li]; });
+        } else {
+          const uint64_t* sv = reinterpret_cast<const uint64_t*>(st + a.off_r[c]) + rsh8;
+          uint64_t* dv = static_cast<uint64_t*>(a.r_dst[c]);
+          each([&](uint64_t oo, uint32_t li, uint32_t) { dv[oo] = sv[li]; });
+        }
+      }
+      for (int c = 0; c < a.ns_cols; ++c) {
+        if (a.s_bytes[c] == 4) {
+          const uint32_t* sv = reinterpret_cast<const uint32_t*>(st + a.off_s[c]) + ssh4;
+          uint32_t* dv = static_cast<uint32_t*>(a.s_dst[c]);
+          each([&](uint64_t oo, uint32_t, uint32_t jl) { dv[oo] = sv[jl]; });
+        } else {
+          const uint64_t* sv = reinterpret_cast<const uint64_t*>(st + a.off_s[c]) + ssh8;
+          uint64_t* dv = static_cast<uint64_t*>(a.s_dst[c]);
+          each([&](uint64_t oo, uint32_t, uint32_t jl) { dv[oo] = sv[jl]; });
+        }
+      }
+      __syncthreads();
+      continue;
+    }
+    // general: per probe, its whole r run (probe rows in rounds of 32)
+    const uint32_t rounds = (nq + 31) / 32;
+    const uint32_t r0 = rounds * warp / kTmaWarps, r1 = rounds * (warp + 1) / kTmaWarps;
     uint64_t o = s_wbase[warp];
     for (uint32_t rr = r0; rr < r1; ++rr) {
       const uint32_t jl = rr * 32 + lane;
@@ -436,8 +573,13 @@ size_t smj_layout_w(SmjArgs& a, bool write, uint32_t wmax) {
       a.off_s[c] = (uint32_t)off;
       off = up(off + (size_t)(kTileS + 8) * a.s_bytes[c]);
     }
+  if (write && a.match_e) {
+    a.off_e = (uint32_t)off;
+    off = up(off + (size_t)(kTileS + 8) * 2);
+  }
   a.stage_bytes = (uint32_t)off;
-  return 2 * off + 2 * sizeof(uint32_t) * kTileS;
+  // loff + mcnt [kTileS] each, list [kSmjList] (fill)
+  return 2 * off + 2 * sizeof(uint32_t) * kTileS + (write ? sizeof(uint32_t) * kSmjList : 0);
 }
 
 // Largest r window (shared-memory keys + R payloads) whose two stages fit.
@@ -459,6 +601,14 @@ uint64_t run_tma(cj_ctx* ctx, SmjArgs a) {
   if (a.tiles == 0 || a.nr == 0) return 0;
   Scratch desc(ctx, a.tiles * sizeof(SmjDesc)), counts(ctx, a.tiles * 8), offs(ctx, a.tiles * 8);
   a.desc = desc.p;
+  // PK-FK: the count pass hands every probe's window index to the fill pass
+  const char* he = std::getenv("CJ_FIND_HANDOFF");
+  const bool handoff = a.write && a.pk_fk && a.padded && !(he && std::strcmp(he, "0") == 0);
+  Scratch me(ctx, handoff ? a.ns * 2 + kPad : 0), pre(ctx, handoff ? a.tiles + 16 : 0);
+  if (handoff) {
+    a.match_e = me.as<uint16_t>();
+    a.tile_pre = pre.as<uint8_t>();
+  }
   ctx->kbegin("smj_bounds", a.tiles * (2 * sizeof(K) + 32));
   k_smj_bounds<K><<<grid_for(a.tiles, 128, 4096), 128, 0, ctx->stream>>>(
       static_cast<const K*>(a.r), a.nr, static_cast<const K*>(a.s), a.ns, a.tiles,
@@ -470,8 +620,13 @@ uint64_t run_tma(cj_ctx* ctx, SmjArgs a) {
   const unsigned grid = (unsigned)std::min<uint64_t>((uint64_t)ctx->num_sms, a.tiles);
   CJ_CUDA(cudaFuncSetAttribute(k_smj_tma<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem_c));
+  int per_sm = 1;
+  CJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_smj_tma<K, false>, kTmaThreads,
+                                                        smem_c));
+  const unsigned grid_c = (unsigned)std::min<uint64_t>(
+      (uint64_t)ctx->num_sms * std::max(1, std::min(per_sm, 2)), a.tiles);
   ctx->kbegin("smj_count", sizeof(K) * (a.nr + a.ns));
-  k_smj_tma<K, false><<<grid, kTmaThreads, smem_c, ctx->stream>>>(ac);
+  k_smj_tma<K, false><<<grid_c, kTmaThreads, smem_c, ctx->stream>>>(ac);
   ctx->kend();
   scan_counts(ctx, counts.as<uint64_t>(), a.tiles, offs.as<uint64_t>(), tot.as<uint64_t>());
   CJ_CUDA(cudaGetLastError());

@@ -1,7 +1,8 @@
 cd $GRAFT_REPO_ROOT
-timeout 300 python -m pytest tests/test_gpu_parity.py -x -q -k "radix or sort or partition or run_join or shard" 2>&1 | tail -2
-for e in "CJ_RANK=0" "CJ_RANK=1" "CJ_RANK=0 CJ_SCATTER_ITEMS=4" "CJ_SCATTER_V=2"; do
-  echo "== $e"
-  env $e timeout 60 python tools_part.py 2>&1 | tail -1
+timeout 900 python -m pytest tests -q -m gpu 2>&1 | tail -2
+timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; head -c 1500 gpurun_out/bench.json; echo; tail -3 gpurun_out/bench.err
+timeout 300 python bench.py --variant smj-gftr --no-extras > gpurun_out/bench_smj.json 2>>gpurun_out/bench.err; head -c 600 gpurun_out/bench_smj.json
+for v in phj-gftr smj-gftr; do
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$v.csv python bench.py --steps 2 --warmup 1 --no-extras --variant $v > /dev/null 2>&1
 done
-timeout 120 python tools_diag.py phj-gftr smj-gftr 2>&1 | grep -E " 3 " | cut -c1-220
+KERNELS="k_scatter_v2" SKIP=2 COUNT=2 bash tools_prof.sh > /dev/null 2>&1
