@@ -170,12 +170,12 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
       : "memory");
 }
 
-// Stable in-warp peers of an 8-bit (or narrower) digit by bit ballots: the
+// Stable in-warp peers of a 9-bit (or narrower) digit by bit ballots: the
 // lanes holding the same digit, restricted to `valid` lanes.
 __device__ __forceinline__ uint32_t digit_peers(uint32_t d, uint32_t bits, uint32_t valid) {
   uint32_t peers = valid;
 #pragma unroll
-  for (uint32_t b = 0; b < 8; ++b) {
+  for (uint32_t b = 0; b < 9; ++b) {
     if (b < bits) {
       const bool set = (d >> b) & 1u;
       const uint32_t bal = __ballot_sync(0xffffffffu, set);

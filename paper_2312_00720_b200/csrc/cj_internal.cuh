@@ -115,9 +115,10 @@ struct ScatterGeom {
   bool tma = false;  // all inputs 16-byte aligned (TMA bulk copies)
   int ctas_per_sm = 2, stages = 2;
   int rank = 0;      // in-warp peer search: 0 atomic-OR masks, 1 ballots
+  int rb = 8;        // digit bits of the passes (8, or 9 for wide full-width sorts)
 };
 ScatterGeom scatter_geom(cj_ctx* ctx, uint64_t n, int key_bytes, const ValCols& vals,
-                         const void* keys_in);
+                         const void* keys_in, int rb = 8);
 
 // Per-block digit counts (cnt[b][p][256]) of every pass of `plan` (<= 8) in one
 // read of the keys, over the blocks of geometry g.
@@ -157,6 +158,10 @@ void partition_offsets(cj_ctx* ctx, const void* keys_sorted, uint64_t n, int key
 
 void copy_columns(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, int key_bytes,
                   const ValCols& vals);
+
+// Plan of a stable full-width sort over the keys' significant bits (8- or
+// 9-bit digits, whichever needs fewer passes).
+PassPlan sort_plan(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes, const ValCols& vals);
 
 // ---- gather.cu ----------------------------------------------------------------
 void gather_cols(cj_ctx* ctx, const void* const* in, uint64_t n_in, const uint32_t* map,

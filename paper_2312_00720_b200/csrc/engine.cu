@@ -121,6 +121,27 @@ PassPlan plan_bits(unsigned total_bits, unsigned per_pass) {  // task.hpp:54-63
 
 PassPlan full_width_plan(int key_bytes) { return plan_bits((unsigned)key_bytes * 8, 8); }
 
+// The device plan for a partition over [0, total_bits): the stable LSD result
+// does not depend on how the bits are split into passes, so the split is a
+// performance choice — at least ceil(total / per_pass) passes of balanced width
+// (narrower digits scatter faster per pass: profiles/r01d_summary.md).
+PassPlan device_plan(unsigned total_bits, unsigned per_pass) {
+  if (per_pass == 0 || per_pass > 8) fail(CJ_ERR_FANOUT_TOO_LARGE, "bits per pass must be in [1, 8]");
+  unsigned np = (total_bits + per_pass - 1) / per_pass;
+  if (const char* e = std::getenv("CJ_PHJ_PASSES")) np = std::max(np, (unsigned)std::atoi(e));
+  np = std::min(np, std::max(total_bits, 1u));
+  PassPlan p;
+  unsigned lo = 0;
+  for (unsigned i = 0; i < np && i < CJ_MAX_PASSES * 3; ++i) {
+    const unsigned w = (total_bits - lo + (np - i) - 1) / (np - i);
+    p.lo[p.npasses] = lo;
+    p.hi[p.npasses] = lo + w;
+    ++p.npasses;
+    lo += w;
+  }
+  return p;
+}
+
 void check_key_bytes(uint32_t kb) {
   if (kb != 4 && kb != 8) fail(CJ_ERR_KIND, "key must be a 4- or 8-byte integer column");
 }
@@ -210,14 +231,14 @@ Side transform(cj_ctx* ctx, const cj_relation* rel, int algo, bool gfur, unsigne
   }
   for (int c = 0; c < v.n; ++c) s.cols[c] = v.out[c];
   if (algo == CJ_SMJ) {
-    lsd_any(ctx, rel->key, s.keys, n, kb, full_width_plan(kb), v);
+    lsd_any(ctx, rel->key, s.keys, n, kb, sort_plan(ctx, rel->key, n, kb, v), v);
   } else {
     s.offsets = static_cast<uint64_t*>(ctx->alloc(sizeof(uint64_t) * ((1ull << total_bits) + 1)));
     owned.push_back(s.offsets);
     if (total_bits == 0) {
       copy_columns(ctx, rel->key, s.keys, n, kb, v);
     } else {
-      lsd_any(ctx, rel->key, s.keys, n, kb, plan_bits(total_bits, bits_per_pass), v);
+      lsd_any(ctx, rel->key, s.keys, n, kb, device_plan(total_bits, bits_per_pass), v);
     }
     partition_offsets(ctx, s.keys, n, kb, total_bits, s.offsets);
   }
@@ -814,7 +835,7 @@ int cj_sort_pairs(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, uin
   return cj::guarded(ctx, [&] {
     cj::check_key_bytes(kb);
     cj::ValCols v = make_vals(vin, vout, vbytes, nvals, gen_ids);
-    cj::lsd_partition(ctx, keys, keys_out, n, (int)kb, cj::full_width_plan((int)kb), v);
+    cj::lsd_partition(ctx, keys, keys_out, n, (int)kb, cj::sort_plan(ctx, keys, n, (int)kb, v), v);
     CJ_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }

@@ -639,6 +639,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constan
     __syncthreads();
 
     // 1. insert chunk positions (CAS); meeting an equal key marks duplicates
+    //    (a plain-store first round measured slower: profiles/r01b_summary.md)
     bool dup = false;
     for (uint32_t i = tid; i < nb; i += kTmaThreads) {
       const K k = bk[i];

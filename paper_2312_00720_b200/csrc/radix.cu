@@ -45,15 +45,29 @@ struct HistArgs {
   uint32_t shift[8], mask[8];
 };
 
-template <class K, int NP, bool SHARD>
+// Digit width: 8 bits (256 digits) everywhere, or 9 bits (512) for the
+// full-width sorts where it saves a pass (see lsd_partition).
+template <int RB> struct Radix {
+  static constexpr int kR = 1 << RB;
+};
+
+// Histogram copies per CTA: one per warp while the copies fit 64 KB, else 4.
+template <int NP, int RB>
+constexpr int hist_copies() {
+  return NP * (1 << RB) * kHistWarps * 4 <= 64 * 1024 ? kHistWarps : 4;
+}
+
+template <class K, int NP, bool SHARD, int RB>
 __global__ void __launch_bounds__(kHistThreads)
 k_block_hist(const K* __restrict__ keys, const __grid_constant__ HistArgs a,
              uint32_t* __restrict__ cnt) {
-  extern __shared__ uint32_t sh[];  // [warp][NP * 256]
-  constexpr int kWidth = NP * kRadix;
-  for (int i = threadIdx.x; i < kHistWarps * kWidth; i += kHistThreads) sh[i] = 0;
+  extern __shared__ uint32_t sh[];  // [copy][NP * R]
+  constexpr int kR = Radix<RB>::kR;
+  constexpr int kWidth = NP * kR;
+  constexpr int kCopies = hist_copies<NP, RB>();
+  for (int i = threadIdx.x; i < kCopies * kWidth; i += kHistThreads) sh[i] = 0;
   __syncthreads();
-  uint32_t* mine = sh + (threadIdx.x >> 5) * kWidth;
+  uint32_t* mine = sh + ((threadIdx.x >> 5) % kCopies) * kWidth;
   // gridDim.x = nblocks * kHistSub: sub-CTA s of block b counts a quarter of
   // the block's tiles and adds into cnt[b] (zeroed by the caller)
   const uint64_t b = blockIdx.x / kHistSub, sub = blockIdx.x % kHistSub;
@@ -71,7 +85,7 @@ k_block_hist(const K* __restrict__ keys, const __grid_constant__ HistArgs a,
       atomicAdd(&mine[(uint32_t)__umul64hi(dev::mix64((uint64_t)k), (uint64_t)a.hparts)], 1u);
     } else {
 #pragma unroll
-      for (int p = 0; p < NP; ++p) atomicAdd(&mine[p * kRadix + ((uint32_t)(k >> shf[p]) & msk[p])], 1u);
+      for (int p = 0; p < NP; ++p) atomicAdd(&mine[p * kR + ((uint32_t)(k >> shf[p]) & msk[p])], 1u);
     }
   };
   constexpr int kVec = 16 / sizeof(K);
@@ -106,50 +120,52 @@ k_block_hist(const K* __restrict__ keys, const __grid_constant__ HistArgs a,
   for (int d = threadIdx.x; d < kWidth; d += kHistThreads) {
     uint32_t t = 0;
 #pragma unroll
-    for (int w = 0; w < kHistWarps; ++w) t += sh[w * kWidth + d];
+    for (int w = 0; w < kCopies; ++w) t += sh[w * kWidth + d];
     if (t) atomicAdd(&cnt[b * kWidth + d], t);
   }
 }
 
-template <class K, int NP, bool SHARD>
+template <class K, int NP, bool SHARD, int RB>
 void launch_hist(cj_ctx* ctx, const K* keys, const HistArgs& a, uint32_t* cnt) {
-  const size_t smem = sizeof(uint32_t) * kRadix * NP * kHistWarps;
-  CJ_CUDA(cudaFuncSetAttribute(k_block_hist<K, NP, SHARD>,
+  const size_t smem = sizeof(uint32_t) * (1 << RB) * NP * hist_copies<NP, RB>();
+  CJ_CUDA(cudaFuncSetAttribute(k_block_hist<K, NP, SHARD, RB>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_block_hist<K, NP, SHARD><<<a.nblocks * kHistSub, kHistThreads, smem, ctx->stream>>>(keys, a, cnt);
+  k_block_hist<K, NP, SHARD, RB><<<a.nblocks * kHistSub, kHistThreads, smem, ctx->stream>>>(keys, a,
+                                                                                           cnt);
 }
 
-template <class K>
+template <class K, int RB>
 void launch_hist_np(cj_ctx* ctx, const K* keys, const HistArgs& a, int np, uint32_t* cnt) {
-  if (a.hparts) return launch_hist<K, 1, true>(ctx, keys, a, cnt);
+  if (a.hparts) return launch_hist<K, 1, true, 8>(ctx, keys, a, cnt);
   switch (np) {
-    case 1: return launch_hist<K, 1, false>(ctx, keys, a, cnt);
-    case 2: return launch_hist<K, 2, false>(ctx, keys, a, cnt);
-    case 3: return launch_hist<K, 3, false>(ctx, keys, a, cnt);
-    case 4: return launch_hist<K, 4, false>(ctx, keys, a, cnt);
-    case 5: return launch_hist<K, 5, false>(ctx, keys, a, cnt);
-    case 6: return launch_hist<K, 6, false>(ctx, keys, a, cnt);
-    case 7: return launch_hist<K, 7, false>(ctx, keys, a, cnt);
-    default: return launch_hist<K, 8, false>(ctx, keys, a, cnt);
+    case 1: return launch_hist<K, 1, false, RB>(ctx, keys, a, cnt);
+    case 2: return launch_hist<K, 2, false, RB>(ctx, keys, a, cnt);
+    case 3: return launch_hist<K, 3, false, RB>(ctx, keys, a, cnt);
+    case 4: return launch_hist<K, 4, false, RB>(ctx, keys, a, cnt);
+    case 5: return launch_hist<K, 5, false, RB>(ctx, keys, a, cnt);
+    case 6: return launch_hist<K, 6, false, RB>(ctx, keys, a, cnt);
+    case 7: return launch_hist<K, 7, false, RB>(ctx, keys, a, cnt);
+    default: return launch_hist<K, 8, false, RB>(ctx, keys, a, cnt);
   }
 }
 
 // Totals and exclusive digit bases per pass from the per-block counts
-// (1 block of 256 threads; thread d owns digit d).
+// (1 block of R threads; thread d owns digit d).
 __global__ void k_digit_bases(const uint32_t* __restrict__ cnt, uint32_t nblocks, int npasses,
-                              uint32_t* __restrict__ totals, uint64_t* __restrict__ base) {
-  __shared__ uint64_t warp_tot[kRadix / 32];
+                              uint32_t radix, uint32_t* __restrict__ totals,
+                              uint64_t* __restrict__ base) {
+  __shared__ uint64_t warp_tot[512 / 32];
   const int d = threadIdx.x;
   for (int p = 0; p < npasses; ++p) {
     uint64_t c = 0;
-    for (uint32_t b = 0; b < nblocks; ++b) c += cnt[((uint64_t)b * npasses + p) * kRadix + d];
-    totals[p * kRadix + d] = (uint32_t)c;
+    for (uint32_t b = 0; b < nblocks; ++b) c += cnt[((uint64_t)b * npasses + p) * radix + d];
+    totals[p * radix + d] = (uint32_t)c;
     const uint64_t inc = dev::warp_inclusive_sum(c);
     if ((d & 31) == 31) warp_tot[d >> 5] = inc;
     __syncthreads();
     uint64_t off = 0;
     for (int w = 0; w < (d >> 5); ++w) off += warp_tot[w];
-    base[p * kRadix + d] = off + inc - c;
+    base[p * radix + d] = off + inc - c;
     __syncthreads();
   }
 }
@@ -449,13 +465,14 @@ __device__ __forceinline__ uint32_t digit_of(K k, const BlockPassArgs& a) {
 }
 
 // One tile of k_scatter_v2 (phases 1-4).  FULL: tile_n == kTile, no guards.
-template <class K, int ITEMS, int RANK, bool SHARD, bool FULL>
+template <class K, int ITEMS, int RANK, bool SHARD, bool FULL, int RB>
 __device__ __forceinline__ void scatter_tile(const BlockPassArgs& a, const uint8_t* st,
-                                             uint16_t* sidx, uint16_t (*whist)[kRadix],
+                                             uint16_t* sidx, uint16_t (*whist)[1 << RB],
                                              uint32_t* mm, uint32_t* dstart, uint32_t* run,
                                              uint32_t* goff, uint32_t* wsum, uint32_t tbase,
                                              uint32_t tile_n) {
   constexpr uint32_t kTile = ITEMS * kTmaThreads;
+  constexpr int kR = 1 << RB;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const K* skey = reinterpret_cast<const K*>(st);
 #ifdef CJ_PHASE_CLOCKS
@@ -480,7 +497,7 @@ __device__ __forceinline__ void scatter_tile(const BlockPassArgs& a, const uint8
       if (RANK == 0) mm[d] = 0;
     }
     old = __shfl_sync(0xffffffffu, old, __ffs(peers | (1u << lane)) - 1);
-    pk[i] = valid ? ((old + __popc(lt)) << 8) | d : 0xffffffffu;
+    pk[i] = valid ? ((old + __popc(lt)) << RB) | d : 0xffffffffu;
     if (RANK == 0) __syncwarp();
   }
   __syncthreads();
@@ -490,7 +507,7 @@ __device__ __forceinline__ void scatter_tile(const BlockPassArgs& a, const uint8
   //    of warp w's first row of digit d (digit start + earlier warps' counts)
   {
     uint32_t c[kTmaWarps], r = 0, inc = 0;
-    if (tid < kRadix) {
+    if (tid < kR) {
 #pragma unroll
       for (int w = 0; w < kTmaWarps; ++w) {
         c[w] = whist[w][tid];
@@ -501,10 +518,10 @@ __device__ __forceinline__ void scatter_tile(const BlockPassArgs& a, const uint8
     }
     __syncthreads();
     CJ_CLK(2);
-    if (tid < kRadix) {
+    if (tid < kR) {
       uint32_t off = 0;
 #pragma unroll
-      for (int w = 0; w < kRadix / 32; ++w) off += w < warp ? wsum[w] : 0;
+      for (int w = 0; w < kR / 32; ++w) off += w < warp ? wsum[w] : 0;
       const uint32_t ds = off + inc - r;
       uint32_t p = ds;
 #pragma unroll
@@ -523,7 +540,7 @@ __device__ __forceinline__ void scatter_tile(const BlockPassArgs& a, const uint8
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     if (FULL || pk[i] != 0xffffffffu) {
-      sidx[wh[pk[i] & 0xffu] + (pk[i] >> 8)] = (uint16_t)(wseg + i * 32 + lane);
+      sidx[wh[pk[i] & (kR - 1)] + (pk[i] >> RB)] = (uint16_t)(wseg + i * 32 + lane);
     }
   }
   __syncthreads();
@@ -575,19 +592,22 @@ __device__ __forceinline__ void scatter_tile(const BlockPassArgs& a, const uint8
   (void)kTile;
 }
 
-template <class K, int ITEMS, int RANK, bool SHARD, int MINB>
+template <class K, int ITEMS, int RANK, bool SHARD, int MINB, int RB>
 __global__ void __launch_bounds__(kTmaThreads, MINB)
 k_scatter_v2(const __grid_constant__ BlockPassArgs a) {
   constexpr uint32_t kTile = ITEMS * kTmaThreads;
+  constexpr int kR = 1 << RB;
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* const stage0 = smem;
   uint16_t* const sidx = reinterpret_cast<uint16_t*>(smem + (size_t)a.stages * a.stage_bytes);
-  __shared__ uint16_t whist[kTmaWarps][kRadix];
-  __shared__ uint32_t match_word[RANK == 0 ? kTmaWarps : 1][kRadix];
-  __shared__ uint32_t dstart[kRadix];
-  __shared__ uint32_t run[kRadix];   // next global row of each digit in this block
-  __shared__ uint32_t goff[kRadix];  // global row of tile slot 0 of each digit's run (mod 2^32)
-  __shared__ uint32_t wsum[kRadix / 32];
+  // per-warp peer masks (rank mode 0) after the source indices, 16-byte aligned
+  uint32_t (*match_word)[kR] = reinterpret_cast<uint32_t (*)[kR]>(
+      smem + (((size_t)a.stages * a.stage_bytes + (size_t)kTile * 2 + 15) & ~size_t(15)));
+  __shared__ uint16_t whist[kTmaWarps][kR];
+  __shared__ uint32_t dstart[kR];
+  __shared__ uint32_t run[kR];   // next global row of each digit in this block
+  __shared__ uint32_t goff[kR];  // global row of tile slot 0 of each digit's run (mod 2^32)
+  __shared__ uint32_t wsum[kR / 32];
   __shared__ __align__(8) uint64_t mbar[2];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -617,8 +637,8 @@ k_scatter_v2(const __grid_constant__ BlockPassArgs a) {
     if (t_begin < t_end && full_tile(t_begin)) issue(0, t_begin);
   }
   if (RANK == 0)
-    for (int i = tid; i < kTmaWarps * kRadix; i += kTmaThreads) (&match_word[0][0])[i] = 0;
-  if (tid < kRadix) {
+    for (int i = tid; i < kTmaWarps * kR; i += kTmaThreads) (&match_word[0][0])[i] = 0;
+  if (tid < kR) {
     uint64_t c = a.base[tid];
     for (uint64_t b2 = 0; b2 < blk; ++b2) c += a.cnt[b2 * a.cnt_stride + tid];
     run[tid] = (uint32_t)c;
@@ -638,7 +658,7 @@ k_scatter_v2(const __grid_constant__ BlockPassArgs a) {
     {
       uint32_t* wrow = reinterpret_cast<uint32_t*>(&whist[warp][0]);
 #pragma unroll
-      for (int i = 0; i < kRadix / 2 / 32; ++i) wrow[lane + 32 * i] = 0;
+      for (int i = 0; i < kR / 2 / 32; ++i) wrow[lane + 32 * i] = 0;
       __syncwarp();
     }
     const uint64_t tbase = t * kTile;
@@ -647,7 +667,7 @@ k_scatter_v2(const __grid_constant__ BlockPassArgs a) {
     if (full_tile(t)) {
       dev::mbar_wait(&mbar[b], b ? ph1 : ph0);
       if (b) ph1 ^= 1; else ph0 ^= 1;
-      scatter_tile<K, ITEMS, RANK, SHARD, true>(a, st, sidx, whist, mm, dstart, run, goff, wsum,
+      scatter_tile<K, ITEMS, RANK, SHARD, true, RB>(a, st, sidx, whist, mm, dstart, run, goff, wsum,
                                                 (uint32_t)tbase, tile_n);
     } else {  // last, partial tile: plain loads
       K* wk = reinterpret_cast<K*>(st);
@@ -665,7 +685,7 @@ k_scatter_v2(const __grid_constant__ BlockPassArgs a) {
         }
       }
       __syncthreads();
-      scatter_tile<K, ITEMS, RANK, SHARD, false>(a, st, sidx, whist, mm, dstart, run, goff, wsum,
+      scatter_tile<K, ITEMS, RANK, SHARD, false, RB>(a, st, sidx, whist, mm, dstart, run, goff, wsum,
                                                  (uint32_t)tbase, tile_n);
     }
     __syncthreads();
@@ -676,21 +696,22 @@ k_scatter_v2(const __grid_constant__ BlockPassArgs a) {
   }
 }
 
-template <class K, int ITEMS, int RANK, int MINB>
+template <class K, int ITEMS, int RANK, int MINB, int RB>
 void launch_v2(cj_ctx* ctx, const BlockPassArgs& a, size_t smem) {
-  auto kern = a.hparts ? k_scatter_v2<K, ITEMS, RANK, true, MINB>
-                       : k_scatter_v2<K, ITEMS, RANK, false, MINB>;
+  auto kern = a.hparts ? k_scatter_v2<K, ITEMS, RANK, true, MINB, 8>
+                       : k_scatter_v2<K, ITEMS, RANK, false, MINB, RB>;
   CJ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<a.nblocks, kTmaThreads, smem, ctx->stream>>>(a);
 }
 
 template <class K, int RANK>
-void launch_v2_items(cj_ctx* ctx, const BlockPassArgs& a, size_t smem, int items) {
+void launch_v2_items(cj_ctx* ctx, const BlockPassArgs& a, size_t smem, int items, int rb) {
+  if (rb != 8) fail(CJ_ERR_UNSUPPORTED, "scatter pass digits wider than 8 bits");
   switch (items) {
-    case 16: launch_v2<K, 16, RANK, 1>(ctx, a, smem); break;
-    case 12: launch_v2<K, 12, RANK, 1>(ctx, a, smem); break;
-    case 8: launch_v2<K, 8, RANK, 1>(ctx, a, smem); break;
-    default: launch_v2<K, 4, RANK, 1>(ctx, a, smem); break;
+    case 16: launch_v2<K, 16, RANK, 1, 8>(ctx, a, smem); break;
+    case 12: launch_v2<K, 12, RANK, 1, 8>(ctx, a, smem); break;
+    case 8: launch_v2<K, 8, RANK, 1, 8>(ctx, a, smem); break;
+    default: launch_v2<K, 4, RANK, 1, 8>(ctx, a, smem); break;
   }
 }
 
@@ -710,8 +731,9 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 }  // namespace
 
 ScatterGeom scatter_geom(cj_ctx* ctx, uint64_t n, int key_bytes, const ValCols& vals,
-                         const void* keys_in) {
+                         const void* keys_in, int rb) {
   ScatterGeom g;
+  g.rb = rb;
   uint64_t row = key_bytes;
   uint32_t maxw = key_bytes;
   bool al = aligned16(keys_in);
@@ -733,16 +755,19 @@ ScatterGeom scatter_geom(cj_ctx* ctx, uint64_t n, int key_bytes, const ValCols& 
   g.ctas_per_sm = 1;  // (2 CTAs/SM with single stages measured slower: profiles/)
   g.stages = e_stages ? std::min(2, std::max(1, std::atoi(e_stages))) : 2;
   const int want_items = e_items ? std::atoi(e_items) : 12;
-  // 227 KB per CTA minus the static arrays (whist 8 KB, match words 16 KB for
-  // rank mode 0, ~3 KB of cursors)
-  const size_t budget = (size_t)(227 - (g.rank == 0 ? 28 : 12)) * 1024;
+  // 227 KB per CTA minus the static arrays (per-warp digit counts 8 KB and
+  // ~4 KB of cursors, twice that for 9-bit digits) and the dynamic peer masks
+  // of rank mode 0 (16 KB / 32 KB)
+  const size_t budget = (227 - ((size_t)12 << (rb - 8))) * 1024;
+  const size_t match = g.rank == 0 ? (size_t)kTmaWarps * 4 << rb : 0;
   for (int items : {16, 12, 8, 4}) {
     if (items > want_items && items > 4) continue;
+    if (rb == 9 && items > 12) continue;
     g.items = items;
     g.tile = (uint64_t)kTmaThreads * items;
     g.stage_bytes = (uint32_t)(g.tile * row);
     g.pbytes = 0;
-    g.smem = (size_t)g.stages * g.stage_bytes + g.tile * 2;
+    g.smem = (((size_t)g.stages * g.stage_bytes + g.tile * 2 + 15) & ~size_t(15)) + match;
     if (g.smem <= budget) break;
   }
   if (g.smem > budget) g.tma = false;  // rows too wide: the look-back onesweep path
@@ -770,12 +795,14 @@ void block_hist(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes, const 
     a.shift[p] = plan.lo[p];
     a.mask[p] = (1u << (plan.hi[p] - plan.lo[p])) - 1u;
   }
-  CJ_CUDA(cudaMemsetAsync(cnt_dev, 0, sizeof(uint32_t) * kRadix * np * g.nblocks, ctx->stream));
+  const uint32_t R = 1u << g.rb;
+  CJ_CUDA(cudaMemsetAsync(cnt_dev, 0, sizeof(uint32_t) * R * np * g.nblocks, ctx->stream));
   ctx->kbegin("histogram", n * key_bytes);
+  if (g.rb != 8) fail(CJ_ERR_UNSUPPORTED, "histogram digits wider than 8 bits");
   if (key_bytes == 4)
-    launch_hist_np<uint32_t>(ctx, static_cast<const uint32_t*>(keys), a, np, cnt_dev);
+    launch_hist_np<uint32_t, 8>(ctx, static_cast<const uint32_t*>(keys), a, np, cnt_dev);
   else
-    launch_hist_np<uint64_t>(ctx, static_cast<const uint64_t*>(keys), a, np, cnt_dev);
+    launch_hist_np<uint64_t, 8>(ctx, static_cast<const uint64_t*>(keys), a, np, cnt_dev);
   ctx->kend();
   CJ_CUDA(cudaGetLastError());
 }
@@ -787,16 +814,17 @@ void histogram_passes(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes,
   const int np = plan.npasses;
   if (np > 8) fail(CJ_ERR_UNSUPPORTED, "histogram of more than 8 passes");
   block_hist(ctx, keys, n, key_bytes, plan, g, cnt_dev, hparts);
-  ctx->kbegin("digit_bases", 12ull * kRadix * np);
-  k_digit_bases<<<1, kRadix, 0, ctx->stream>>>(cnt_dev, g.nblocks, np, totals_dev, base_dev);
+  const uint32_t R = 1u << g.rb;
+  ctx->kbegin("digit_bases", 12ull * R * np);
+  k_digit_bases<<<1, R, 0, ctx->stream>>>(cnt_dev, g.nblocks, np, R, totals_dev, base_dev);
   ctx->kend();
   CJ_CUDA(cudaGetLastError());
   if (totals_host) {
-    totals_host->resize((size_t)kRadix * np);
-    CJ_CUDA(cudaMemcpyAsync(ctx->host_pinned, totals_dev, sizeof(uint32_t) * kRadix * np,
+    totals_host->resize((size_t)R * np);
+    CJ_CUDA(cudaMemcpyAsync(ctx->host_pinned, totals_dev, sizeof(uint32_t) * R * np,
                             cudaMemcpyDeviceToHost, ctx->stream));
     CJ_CUDA(cudaStreamSynchronize(ctx->stream));
-    std::memcpy(totals_host->data(), ctx->host_pinned, sizeof(uint32_t) * kRadix * np);
+    std::memcpy(totals_host->data(), ctx->host_pinned, sizeof(uint32_t) * R * np);
   }
 }
 
@@ -837,11 +865,11 @@ void scatter_pass(cj_ctx* ctx, const void* keys_in, void* keys_out, uint64_t n, 
     }
     ctx->kbegin("scatter_pass", n * (row + wrow));
     if (key_bytes == 4) {
-      if (g.rank == 1) launch_v2_items<uint32_t, 1>(ctx, a, g.smem, g.items);
-      else launch_v2_items<uint32_t, 0>(ctx, a, g.smem, g.items);
+      if (g.rank == 1) launch_v2_items<uint32_t, 1>(ctx, a, g.smem, g.items, g.rb);
+      else launch_v2_items<uint32_t, 0>(ctx, a, g.smem, g.items, g.rb);
     } else {
-      if (g.rank == 1) launch_v2_items<uint64_t, 1>(ctx, a, g.smem, g.items);
-      else launch_v2_items<uint64_t, 0>(ctx, a, g.smem, g.items);
+      if (g.rank == 1) launch_v2_items<uint64_t, 1>(ctx, a, g.smem, g.items, g.rb);
+      else launch_v2_items<uint64_t, 0>(ctx, a, g.smem, g.items, g.rb);
     }
     ctx->kend();
     CJ_CUDA(cudaGetLastError());
@@ -939,7 +967,12 @@ void lsd_partition_group(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t
                          std::vector<uint32_t>* counts_out) {
   if (plan.npasses > 8) fail(CJ_ERR_UNSUPPORTED, "LSD segment longer than 8 passes");
   const int np = plan.npasses;
-  const ScatterGeom g0 = scatter_geom(ctx, n, key_bytes, vals, keys);
+  int rb = 8;
+  for (int p = 0; p < np; ++p)
+    if (plan.hi[p] - plan.lo[p] > 8) rb = 9;
+  const uint32_t kRadix = 1u << rb;
+  const ScatterGeom g0 = scatter_geom(ctx, n, key_bytes, vals, keys, rb);
+  if (rb > 8 && !g0.tma) fail(CJ_ERR_UNSUPPORTED, "9-bit digits need the TMA scatter path");
   std::vector<uint32_t> totals;
   Scratch cnt(ctx, sizeof(uint32_t) * kRadix * std::max(np, 1) * g0.nblocks);
   Scratch tot(ctx, sizeof(uint32_t) * kRadix * std::max(np, 1));
@@ -951,7 +984,7 @@ void lsd_partition_group(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t
   for (int p = 0; p < np; ++p) {
     if (plan.hi[p] == plan.lo[p]) continue;
     bool constant = n == 0;
-    for (int d = 0; d < kRadix && !constant; ++d)
+    for (uint32_t d = 0; d < kRadix && !constant; ++d)
       if (totals[(size_t)p * kRadix + d] == n) constant = true;
     if (!constant) live.push_back(p);
   }
@@ -991,7 +1024,7 @@ void lsd_partition_group(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t
                    g0.tma ? cnt.as<uint32_t>() + (size_t)p * kRadix : nullptr,
                    (uint32_t)(kRadix * np), g0, step);
     } else {
-      const ScatterGeom g = scatter_geom(ctx, n, key_bytes, step, cur_k);
+      const ScatterGeom g = scatter_geom(ctx, n, key_bytes, step, cur_k, rb);
       const uint32_t* pc = nullptr;
       if (g.tma) {
         PassPlan one;
@@ -1035,6 +1068,69 @@ void shard_partition(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, 
                  cnt.as<uint32_t>(), kRadix, g, vals, parts);
   for (uint32_t d = 0; d < parts; ++d) counts_host[d] = totals[d];
   CJ_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+namespace {
+template <class K>
+__global__ void k_key_or(const K* __restrict__ keys, uint64_t n, unsigned long long* out) {
+  K acc = 0;
+  constexpr int kVec = 16 / sizeof(K);
+  const uint4* kv = reinterpret_cast<const uint4*>(keys);
+  const uint64_t nvec = n / kVec;
+  for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nvec;
+       v += (uint64_t)gridDim.x * blockDim.x) {
+    const uint4 q = __ldcs(kv + v);
+    K e[kVec];
+    memcpy(e, &q, 16);
+#pragma unroll
+    for (int j = 0; j < kVec; ++j) acc |= e[j];
+  }
+  for (uint64_t i = nvec * kVec + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    acc |= keys[i];
+  uint64_t a64 = (uint64_t)acc;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) a64 |= __shfl_xor_sync(0xffffffffu, a64, o);
+  if ((threadIdx.x & 31) == 0 && a64) atomicOr(out, (unsigned long long)a64);
+}
+}  // namespace
+
+// Stable full-width sort plan (sort_pairs, primitives.cpp:358-362): LSD digits
+// over the significant bits of the keys only (higher bits are zero for every
+// key, so those passes would be constant and skipped anyway), ceil(bits / 8)
+// passes of balanced width — e.g. 27-bit keys: 7+7+7+6 bits, which scatter
+// faster than 8+8+8+3 (fewer digits per pass: longer runs per tile).  9-bit
+// digits (3 passes) measured slower than four narrow passes (r01d).  The stable
+// result is the same for every split.
+PassPlan sort_plan(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes, const ValCols& vals) {
+  uint32_t bits = (uint32_t)key_bytes * 8;
+  if (n > 0 && (reinterpret_cast<uintptr_t>(keys) & 15u) == 0) {
+    Scratch acc(ctx, 8);
+    CJ_CUDA(cudaMemsetAsync(acc.p, 0, 8, ctx->stream));
+    ctx->kbegin("key_bits", n * key_bytes);
+    if (key_bytes == 4)
+      k_key_or<uint32_t><<<grid_for(n / 4, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+          static_cast<const uint32_t*>(keys), n, acc.as<unsigned long long>());
+    else
+      k_key_or<uint64_t><<<grid_for(n / 2, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+          static_cast<const uint64_t*>(keys), n, acc.as<unsigned long long>());
+    ctx->kend();
+    uint64_t* h = reinterpret_cast<uint64_t*>(ctx->host_pinned);
+    CJ_CUDA(cudaMemcpyAsync(h, acc.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CJ_CUDA(cudaStreamSynchronize(ctx->stream));
+    bits = h[0] ? 64u - (uint32_t)__builtin_clzll(h[0]) : 1u;
+  }
+  const uint32_t np = (bits + 7) / 8;
+  PassPlan plan;
+  plan.npasses = (int)np;
+  uint32_t lo = 0;
+  for (uint32_t p = 0; p < np; ++p) {  // balanced widths, each <= 8 (or 9)
+    const uint32_t w = (bits - lo + (np - p) - 1) / (np - p);
+    plan.lo[p] = lo;
+    plan.hi[p] = lo + w;
+    lo += w;
+  }
+  return plan;
 }
 
 void partition_offsets(cj_ctx* ctx, const void* keys_sorted, uint64_t n, int key_bytes,
