@@ -26,6 +26,13 @@ uint64_t cjo_digest(const uint64_t* w, uint64_t n) {
   return h;
 }
 
+/* The same digest fed in pieces: h from the previous piece (0x12345678 for the
+ * first), i0 = number of words already digested. */
+uint64_t cjo_digest_continue(uint64_t h, const uint64_t* w, uint64_t n, uint64_t i0) {
+  for (uint64_t i = 0; i < n; ++i) h = cjo_mix64(h ^ w[i]) + (i0 + i);
+  return h;
+}
+
 /* ---- rng.hpp:18-37 CounterRng ------------------------------------------ */
 typedef struct { uint64_t seed; } rng_t;
 static rng_t rng_make(uint64_t seed) { rng_t r = {seed}; return r; }

@@ -27,6 +27,7 @@ enum { CJO_OK = 0, CJO_FANOUT_TOO_LARGE = 3, CJO_INDEX_OOB = 4, CJO_EMPTY = 5,
 
 uint64_t cjo_mix64(uint64_t x);
 uint64_t cjo_digest(const uint64_t* w, uint64_t n);
+uint64_t cjo_digest_continue(uint64_t h, const uint64_t* w, uint64_t n, uint64_t i0);
 
 /* workloads.cpp:89-133 gen_pk_fk.  Output arrays are caller-allocated:
  * r_key[r_rows], r_pay[r_pay * r_rows] (column-major), same for S.

@@ -42,6 +42,8 @@ def lib():
         L.cjo_mix64.argtypes = [C.c_uint64]
         L.cjo_digest.restype = C.c_uint64
         L.cjo_digest.argtypes = [_u64p, C.c_uint64]
+        L.cjo_digest_continue.restype = C.c_uint64
+        L.cjo_digest_continue.argtypes = [C.c_uint64, _u64p, C.c_uint64, C.c_uint64]
         L.cjo_gen_pk_fk.argtypes = [C.c_uint64, C.c_uint64, C.c_uint, C.c_uint, C.c_double,
                                     C.c_double, C.c_uint64, C.c_uint, _u64p, _u64p, _u64p, _u64p]
         L.cjo_default_total_radix_bits.restype = C.c_uint
@@ -100,6 +102,20 @@ def mix64(x: int) -> int:
 def digest(words) -> int:
     w = _u64(words).ravel()
     return int(lib().cjo_digest(w if w.size else np.zeros(1, np.uint64), w.size))
+
+
+class DigestStream:
+    """digest() of a long word sequence fed in pieces (BASELINE.md §2 formula)."""
+
+    def __init__(self):
+        self.h, self.i = 0x12345678, 0
+
+    def update(self, words):
+        w = np.ascontiguousarray(_u64(words).ravel())
+        if w.size:
+            self.h = int(lib().cjo_digest_continue(self.h, w, w.size, self.i))
+            self.i += w.size
+        return self
 
 
 def default_total_radix_bits(build_rows: int) -> int:

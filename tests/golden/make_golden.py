@@ -11,7 +11,8 @@ Runs oracle/_ref/refjoin (the reference library compiled from
   * prim:  primitive known-answer digests (refjoin.cpp cmd_prim).
 Only runs where /root/reference exists (this container); the JSON is committed.
 
-    python tests/golden/make_golden.py
+    python tests/golden/make_golden.py            # everything
+    python tests/golden/make_golden.py --c2-gen   # append the C2 generator digests only
 """
 import json
 import os
@@ -47,8 +48,25 @@ def wl_args(c):
     return a
 
 
+C2 = dict(r=1 << 27, s=1 << 28, match=1.0, zipf=0.0, key="u32", pay="u32", rpay=2, spay=2,
+          seed=42, name="C2")
+
+
+def add_c2_gen():
+    """Generator digests of the full-size headline config (BASELINE.json configs[1])."""
+    path = os.path.join(HERE, "golden.json")
+    with open(path) as f:
+        out = json.load(f)
+    out["gen"] = [g for g in out["gen"] if g["cell"].get("name") != "C2"]
+    out["gen"].append(dict(cell=C2, digests=O.refjoin("gen", *wl_args(C2))))
+    with open(path, "w") as f:
+        json.dump(out, f, indent=1, sort_keys=True)
+
+
 def main():
     O.build()
+    if "--c2-gen" in sys.argv:
+        return add_c2_gen()
     out = {"join": [], "gen": [], "prim": {}}
     cells = grid()
     cells.append(dict(r=1 << 20, s=1 << 22, match=1.0, zipf=0.0, key="u32", pay="u32", rpay=1,
@@ -73,10 +91,8 @@ def main():
         print(c, file=sys.stderr)
     for c in (cells[0], cells[5], cells[-7], cells[-6], cells[-3]):
         out["gen"].append(dict(cell=c, digests=O.refjoin("gen", *wl_args(c))))
-    c2 = dict(r=1 << 27, s=1 << 28, match=1.0, zipf=0.0, key="u32", pay="u32", rpay=2, spay=2,
-              seed=42, name="C2")
     if os.environ.get("GOLDEN_C2"):
-        out["gen"].append(dict(cell=c2, digests=O.refjoin("gen", *wl_args(c2))))
+        out["gen"].append(dict(cell=C2, digests=O.refjoin("gen", *wl_args(C2))))
     for n, seed in ((5000, 2), (100000, 1)):
         out["prim"][f"{n}:{seed}"] = O.refjoin("prim", "--n", str(n), "--seed", str(seed))
     with open(os.path.join(HERE, "golden.json"), "w") as f:
