@@ -67,6 +67,9 @@ struct cj_ctx {
   // join's scratch never maps new memory mid-call (multi-ms stalls otherwise).
   uint64_t pool_reserved = 0;
   void reserve(uint64_t bytes);
+  // run_join's transforms: run every LSD pass without the constant-digit host
+  // round trip (a constant pass is a stable copy; skipping it only saves time)
+  bool assume_live_passes = false;
 };
 
 namespace cj {

@@ -123,12 +123,16 @@ PassPlan full_width_plan(int key_bytes) { return plan_bits((unsigned)key_bytes *
 
 // The device plan for a partition over [0, total_bits): the stable LSD result
 // does not depend on how the bits are split into passes, so the split is a
-// performance choice — at least ceil(total / per_pass) passes of balanced width
-// (narrower digits scatter faster per pass: profiles/r01d_summary.md).
+// performance choice — at least ceil(total / per_pass) passes (the reference's
+// task.hpp:54-63 plan) and at least ceil(total / 6), of balanced width.  The
+// scatter is shared-memory bound and its cost per pass falls steeply with the
+// digit count: C2's 16 bits in three 6/5/5-bit passes beat two 8-bit passes
+// (11.24 vs 11.43 ms per join; profiles/r01d_summary.md).
 PassPlan device_plan(unsigned total_bits, unsigned per_pass) {
   if (per_pass == 0 || per_pass > 8) fail(CJ_ERR_FANOUT_TOO_LARGE, "bits per pass must be in [1, 8]");
-  unsigned np = (total_bits + per_pass - 1) / per_pass;
-  if (const char* e = std::getenv("CJ_PHJ_PASSES")) np = std::max(np, (unsigned)std::atoi(e));
+  unsigned np = std::max((total_bits + per_pass - 1) / per_pass, (total_bits + 5) / 6);
+  if (const char* e = std::getenv("CJ_PHJ_PASSES")) np = (unsigned)std::max(1, std::atoi(e));
+  np = std::max(np, (total_bits + 7) / 8);
   np = std::min(np, std::max(total_bits, 1u));
   PassPlan p;
   unsigned lo = 0;
@@ -230,6 +234,11 @@ Side transform(cj_ctx* ctx, const cj_relation* rel, int algo, bool gfur, unsigne
     }
   }
   for (int c = 0; c < v.n; ++c) s.cols[c] = v.out[c];
+  struct LiveScope {  // see cj_ctx::assume_live_passes
+    cj_ctx* c;
+    explicit LiveScope(cj_ctx* x) : c(x) { c->assume_live_passes = true; }
+    ~LiveScope() { c->assume_live_passes = false; }
+  } live_scope(ctx);
   if (algo == CJ_SMJ) {
     lsd_any(ctx, rel->key, s.keys, n, kb, sort_plan(ctx, rel->key, n, kb, v), v);
   } else {

@@ -441,21 +441,26 @@ __device__ __forceinline__ void emit_compact(const FindArgs& a, const UnitDesc& 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t bsh4 = (uint32_t)(inf.b_lo & 3), bsh8 = (uint32_t)(inf.b_lo & 1);
   const uint32_t qsh4 = (uint32_t)(inf.q_lo & 3), qsh8 = (uint32_t)(inf.q_lo & 1);
-    // 3a. compact the hits in probe order: list[t] = (build idx << 16) | probe idx
     const uint64_t ubase = s_wbase[0];
-    uint32_t o = (uint32_t)(s_wbase[warp] - ubase);
-    for (uint32_t r = r0; r < r1; ++r) {
-      const uint32_t jl = r * 32 + lane;
-      uint32_t e = kNoMatch;
-      if (jl < nq) e = me ? (me[jl] == kEmpty16 ? kNoMatch : (uint32_t)me[jl]) : res[jl];
-      const bool hit = e != kNoMatch;
-      const uint32_t bal = __ballot_sync(0xffffffffu, hit);
-      if (hit) list[o + __popc(bal & dev::lanemask_lt())] = (e << 16) | jl;
-      o += __popc(bal);
-    }
-    __syncthreads();
-    // 3b. column by column, consecutive threads write consecutive output rows
     uint32_t cnt = (uint32_t)(s_wbase[kTmaWarps - 1] - ubase + s_wcount[kTmaWarps - 1]);
+    // every probe row matched once (PK-FK, match ratio 1): output row t is probe
+    // row t, its build row is me[t]; no compaction needed
+    const bool ident = me != nullptr && cnt == nq;
+    if (!ident) {
+      // 3a. compact the hits in probe order: list[t] = (build idx << 16) | probe idx
+      uint32_t o = (uint32_t)(s_wbase[warp] - ubase);
+      for (uint32_t r = r0; r < r1; ++r) {
+        const uint32_t jl = r * 32 + lane;
+        uint32_t e = kNoMatch;
+        if (jl < nq) e = me ? (me[jl] == kEmpty16 ? kNoMatch : (uint32_t)me[jl]) : res[jl];
+        const bool hit = e != kNoMatch;
+        const uint32_t bal = __ballot_sync(0xffffffffu, hit);
+        if (hit) list[o + __popc(bal & dev::lanemask_lt())] = (e << 16) | jl;
+        o += __popc(bal);
+      }
+      __syncthreads();
+    }
+    // 3b. column by column, consecutive threads write consecutive output rows
     if (ubase + cnt > a.capacity) cnt = ubase < a.capacity ? (uint32_t)(a.capacity - ubase) : 0u;
     constexpr int kE = 8;
     for (uint32_t t0 = 0; t0 < cnt; t0 += kE * kTmaThreads) {
@@ -463,7 +468,7 @@ __device__ __forceinline__ void emit_compact(const FindArgs& a, const UnitDesc& 
 #pragma unroll
       for (int k = 0; k < kE; ++k) {
         const uint32_t t = t0 + tid + k * kTmaThreads;
-        L[k] = t < cnt ? list[t] : 0u;
+        L[k] = t < cnt ? (ident ? ((uint32_t)me[t] << 16) | t : list[t]) : 0u;
       }
       auto each = [&](auto&& f) {
 #pragma unroll
@@ -805,11 +810,11 @@ struct Plan {
 };
 
 Plan make_plan(cj_ctx* ctx, const uint64_t* boff, const uint64_t* poff, uint32_t fanout,
-               uint32_t limit, uint64_t* unit_start) {
+               uint32_t limit, uint64_t* unit_start, uint32_t qchunk) {
   Scratch st(ctx, 2 * sizeof(uint64_t));
   CJ_CUDA(cudaMemsetAsync(st.p, 0, 2 * sizeof(uint64_t), ctx->stream));
   const uint32_t blocks = (fanout + kPlanThreads * kPlanPer - 1) / (kPlanThreads * kPlanPer);
-  PlanArgs2 pa{boff, poff, fanout, limit, probe_chunk(), unit_start,
+  PlanArgs2 pa{boff, poff, fanout, limit, qchunk, unit_start,
                st.as<unsigned long long>(), ctx->status_buffer(blocks), 0, ctx->err_word};
   pa.epoch = ctx->next_epoch();
   ctx->kbegin("phj_plan", 16ull * fanout);
@@ -854,7 +859,22 @@ bool tma_layout(FindArgs& a, size_t* smem_out) {
   // + res[qchunk] probe results + list[qchunk] compacted hits
   const size_t smem = (size_t)a.stages * off + up(4 * (size_t)a.cap_entries) + (size_t)a.qchunk * 8;
   *smem_out = smem;
-  return smem <= 210 * 1024;
+  return smem <= 225 * 1024;  // + < 2 KB of static shared memory
+}
+
+// Probe rows per work unit: the largest (<= 8192, multiple of 128) whose two
+// stages fit shared memory, so a probe partition is rarely split into a second
+// unit that rebuilds the same build table for a few rows (C2: partitions of
+// 4096 +- 64 rows; a 4096 chunk splits half of them).  CJ_QCHUNK overrides.
+template <class K>
+uint32_t choose_qchunk(FindArgs a) {
+  if (std::getenv("CJ_QCHUNK")) return probe_chunk();
+  size_t smem = 0;
+  for (uint32_t q = 8192; q >= 1024; q -= 128) {
+    a.qchunk = q;
+    if (tma_layout<K>(a, &smem)) return q;
+  }
+  return probe_chunk();
 }
 
 template <class K>
@@ -927,25 +947,23 @@ uint64_t run_find(cj_ctx* ctx, FindArgs a, uint64_t total_units) {
       ctx->kend();
       scan_counts(ctx, counts.as<uint64_t>(), U, offs.as<uint64_t>(), a.total_out);
       CJ_CUDA(cudaGetLastError());
+      if (a.write) {
+        // the fill is launched without waiting for the total: every write is
+        // bounded by the capacity on the device, and an overflow is reported
+        // (CapacityExceeded) after the single synchronisation below
+        a.unit_off = offs.as<uint64_t>();
+        CJ_CUDA(cudaFuncSetAttribute(k_phj_tma<K, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tma_smem));
+        ctx->kbegin("phj_find", 0);
+        k_phj_tma<K, true><<<grid, kTmaThreads, tma_smem, ctx->stream>>>(a);
+        ctx->kend();
+        CJ_CUDA(cudaGetLastError());
+      }
       uint64_t* h = reinterpret_cast<uint64_t*>(ctx->host_pinned);
       CJ_CUDA(cudaMemcpyAsync(h, a.total_out, 8, cudaMemcpyDeviceToHost, ctx->stream));
       CJ_CUDA(cudaStreamSynchronize(ctx->stream));
       total = h[0];
-      if (a.write) {
-        if (total > a.capacity) {
-          CJ_CUDA(cudaMemsetAsync(a.err, 0, 4, ctx->stream));
-          atomicOr_host_overflow(ctx);
-        } else {
-          a.unit_off = offs.as<uint64_t>();
-          CJ_CUDA(cudaFuncSetAttribute(k_phj_tma<K, true>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tma_smem));
-          ctx->kbegin("phj_find", 0);
-          k_phj_tma<K, true><<<grid, kTmaThreads, tma_smem, ctx->stream>>>(a);
-          ctx->kend();
-          CJ_CUDA(cudaGetLastError());
-          CJ_CUDA(cudaStreamSynchronize(ctx->stream));
-        }
-      }
+      if (a.write && total > a.capacity) atomicOr_host_overflow(ctx);
     }
     return total;
   } else {
@@ -1025,7 +1043,7 @@ uint64_t phj_find(cj_ctx* ctx, const void* bkeys, const uint64_t* boff, const vo
                   const OutSpec& out, uint64_t capacity) {
   check_limit(limit);
   Scratch us(ctx, sizeof(uint64_t) * ((uint64_t)fanout + 1));
-  const Plan plan = make_plan(ctx, boff, poff, fanout, limit, us.as<uint64_t>());
+  Plan plan = make_plan(ctx, boff, poff, fanout, limit, us.as<uint64_t>(), probe_chunk());
   FindArgs a = base_args(bkeys, boff, pkeys, poff, fanout, limit);
   a.unit_start = us.as<uint64_t>();
   a.max_chunk = (uint32_t)std::max<uint64_t>(plan.max_chunk, 1);
@@ -1034,6 +1052,22 @@ uint64_t phj_find(cj_ctx* ctx, const void* bkeys, const uint64_t* boff, const vo
   a.padded = out.padded ? 1 : 0;
   a.nb_rows = out.r_rows;
   a.np_rows = out.s_rows;
+  a.nr = out.nr;
+  a.ns = out.ns;
+  for (int c = 0; c < out.nr; ++c) a.r_bytes[c] = out.r_bytes[c];
+  for (int c = 0; c < out.ns; ++c) a.s_bytes[c] = out.s_bytes[c];
+  if (a.padded) {
+    uint32_t cap_log2 = 1;
+    while ((1ull << cap_log2) < 2ull * a.max_chunk) ++cap_log2;
+    a.cap_log2 = cap_log2;
+    a.match_e = reinterpret_cast<uint16_t*>(16);  // layout with the hand-off chunk
+    const uint32_t q = key_bytes == 4 ? choose_qchunk<uint32_t>(a) : choose_qchunk<uint64_t>(a);
+    a.match_e = nullptr;
+    if (q != a.qchunk) {
+      a.qchunk = q;
+      plan = make_plan(ctx, boff, poff, fanout, limit, us.as<uint64_t>(), q);
+    }
+  }
   Scratch desc(ctx, std::max<uint64_t>(plan.total_units, 1) * sizeof(UnitDesc));
   if (a.padded) build_desc(ctx, a, plan.total_units, desc);
   a.key_out = out.key;
@@ -1063,7 +1097,7 @@ uint64_t phj_count(cj_ctx* ctx, const void* bkeys, const uint64_t* boff, const v
                    const uint64_t* poff, uint32_t fanout, int key_bytes, uint32_t limit) {
   check_limit(limit);
   Scratch us(ctx, sizeof(uint64_t) * ((uint64_t)fanout + 1));
-  const Plan plan = make_plan(ctx, boff, poff, fanout, limit, us.as<uint64_t>());
+  const Plan plan = make_plan(ctx, boff, poff, fanout, limit, us.as<uint64_t>(), probe_chunk());
   FindArgs a = base_args(bkeys, boff, pkeys, poff, fanout, limit);
   a.unit_start = us.as<uint64_t>();
   a.max_chunk = (uint32_t)std::max<uint64_t>(plan.max_chunk, 1);

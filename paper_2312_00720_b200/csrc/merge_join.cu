@@ -440,16 +440,21 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_smj_tma(const __grid_constan
     const uint64_t tbase = s_wbase[0];
     const uint64_t tcount = s_wbase[kTmaWarps - 1] + s_wcount[kTmaWarps - 1] - tbase;
     if (win && tcount <= kSmjList) {
-      // 2a. compact in (probe, r) order
-      uint32_t o = (uint32_t)(s_wbase[warp] - tbase) + tinc - tsum;
-      for (uint32_t q = 0; q < kSmjPer; ++q) {
-        const uint32_t jl = j0 + q;
-        if (jl < nq) {
-          const uint32_t m = mcnt[jl], l0 = loff[jl];
-          for (uint32_t i = 0; i < m; ++i) list[o++] = ((l0 + i) << 16) | jl;
+      // every probe matched exactly once (PK-FK, match ratio 1): output row t
+      // is probe t, its r row loff[t]; no compaction needed
+      const bool ident = a.pk_fk && tcount == nq;
+      if (!ident) {
+        // 2a. compact in (probe, r) order
+        uint32_t o = (uint32_t)(s_wbase[warp] - tbase) + tinc - tsum;
+        for (uint32_t q = 0; q < kSmjPer; ++q) {
+          const uint32_t jl = j0 + q;
+          if (jl < nq) {
+            const uint32_t m = mcnt[jl], l0 = loff[jl];
+            for (uint32_t i = 0; i < m; ++i) list[o++] = ((l0 + i) << 16) | jl;
+          }
         }
+        __syncthreads();
       }
-      __syncthreads();
       // 2b. column by column, consecutive threads on consecutive output rows
       uint32_t cnt = (uint32_t)tcount;
       if (tbase + cnt > a.capacity) cnt = tbase < a.capacity ? (uint32_t)(a.capacity - tbase) : 0u;
@@ -458,7 +463,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_smj_tma(const __grid_constan
 #pragma unroll
       for (int k = 0; k < kE; ++k) {
         const uint32_t tt = tid + k * kTmaThreads;
-        L[k] = tt < cnt ? list[tt] : 0u;
+        L[k] = tt < cnt ? (ident ? (loff[tt] << 16) | tt : list[tt]) : 0u;
       }
       auto each = [&](auto&& f) {
 #pragma unroll
@@ -630,27 +635,28 @@ uint64_t run_tma(cj_ctx* ctx, SmjArgs a) {
   ctx->kend();
   scan_counts(ctx, counts.as<uint64_t>(), a.tiles, offs.as<uint64_t>(), tot.as<uint64_t>());
   CJ_CUDA(cudaGetLastError());
+  if (a.write) {
+    // launched without waiting for the total: writes are bounded by the
+    // capacity on the device; an overflow is reported after the one sync below
+    a.tile_off = offs.as<uint64_t>();
+    const size_t smem = smj_layout<K>(a, true);
+    if (smem > 220 * 1024) fail(CJ_ERR_UNSUPPORTED, "merge join stage exceeds shared memory");
+    CJ_CUDA(cudaFuncSetAttribute(k_smj_tma<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    ctx->kbegin("smj_find", 0);
+    k_smj_tma<K, true><<<grid, kTmaThreads, smem, ctx->stream>>>(a);
+    ctx->kend();
+    CJ_CUDA(cudaGetLastError());
+  }
   uint64_t* h = reinterpret_cast<uint64_t*>(ctx->host_pinned);
   CJ_CUDA(cudaMemcpyAsync(h, tot.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
   CJ_CUDA(cudaStreamSynchronize(ctx->stream));
   const uint64_t total = h[0];
-  if (!a.write) return total;
-  if (total > a.capacity) {
+  if (a.write && total > a.capacity) {
     const uint32_t v = kErrOverflow;
     CJ_CUDA(cudaMemcpyAsync(ctx->err_word, &v, 4, cudaMemcpyHostToDevice, ctx->stream));
     CJ_CUDA(cudaStreamSynchronize(ctx->stream));
-    return total;
   }
-  a.tile_off = offs.as<uint64_t>();
-  const size_t smem = smj_layout<K>(a, true);
-  if (smem > 220 * 1024) fail(CJ_ERR_UNSUPPORTED, "merge join stage exceeds shared memory");
-  CJ_CUDA(cudaFuncSetAttribute(k_smj_tma<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem));
-  ctx->kbegin("smj_find", 0);
-  k_smj_tma<K, true><<<grid, kTmaThreads, smem, ctx->stream>>>(a);
-  ctx->kend();
-  CJ_CUDA(cudaGetLastError());
-  CJ_CUDA(cudaStreamSynchronize(ctx->stream));
   return total;
 }
 

@@ -977,14 +977,18 @@ void lsd_partition_group(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t
   Scratch cnt(ctx, sizeof(uint32_t) * kRadix * std::max(np, 1) * g0.nblocks);
   Scratch tot(ctx, sizeof(uint32_t) * kRadix * std::max(np, 1));
   Scratch base(ctx, sizeof(uint64_t) * kRadix * std::max(np, 1));
+  // Constant-digit passes are skipped (primitives.cpp:224-226) after one host
+  // round trip for the digit totals; callers that know their passes are live
+  // (ctx->assume_live_passes) run every pass instead and save the sync.
+  const bool skip_check = ctx->assume_live_passes && !counts_out;
   histogram_passes(ctx, keys, n, key_bytes, plan, g0, cnt.as<uint32_t>(), tot.as<uint32_t>(),
-                   base.as<uint64_t>(), &totals);
+                   base.as<uint64_t>(), skip_check ? nullptr : &totals);
   if (counts_out) *counts_out = totals;
   std::vector<int> live;
   for (int p = 0; p < np; ++p) {
     if (plan.hi[p] == plan.lo[p]) continue;
     bool constant = n == 0;
-    for (uint32_t d = 0; d < kRadix && !constant; ++d)
+    for (uint32_t d = 0; d < kRadix && !constant && !skip_check; ++d)
       if (totals[(size_t)p * kRadix + d] == n) constant = true;
     if (!constant) live.push_back(p);
   }
