@@ -35,6 +35,39 @@ METRIC = "end-to-end join throughput (|R|+|S| tuples/s incl. materialisation) vs
 R_ROWS, S_ROWS, NPAY, SEED = 1 << 27, 1 << 28, 2, 42
 WORKLOAD = ("C2: PK-FK |R|=2^27, |S|=2^28, 4-byte key + 2 x 4-byte payloads per relation, "
             "uniform FKs, match ratio 1, seed 42")
+# BASELINE.json configs (C1 is the CPU-sized case, C5 the multi-GPU one)
+CONFIGS = {
+    "C1": dict(r=1 << 20, s=1 << 22, key=4, widths=(4,), match=1.0, zipf=0.0,
+               desc="C1: PK-FK |R|=2^20, |S|=2^22, 4-byte key + 1 x 4-byte payload, uniform, match 1"),
+    "C2": dict(r=R_ROWS, s=S_ROWS, key=4, widths=(4, 4), match=1.0, zipf=0.0, desc=WORKLOAD),
+    "C3": dict(r=R_ROWS, s=S_ROWS, key=8, widths=(4, 8, 4, 8), match=0.5, zipf=0.0,
+               desc="C3: |R|=2^27, |S|=2^28, 8-byte keys + payloads [4,8,4,8] B per relation, "
+                    "match ratio 0.5, seed 42"),
+    "C4z0.5": dict(r=R_ROWS, s=S_ROWS, key=4, widths=(4, 4), match=1.0, zipf=0.5,
+                   desc="C4: C2 with Zipf(0.5) foreign keys"),
+    "C4z1.0": dict(r=R_ROWS, s=S_ROWS, key=4, widths=(4, 4), match=1.0, zipf=1.0,
+                   desc="C4: C2 with Zipf(1.0) foreign keys"),
+    "C4z1.5": dict(r=R_ROWS, s=S_ROWS, key=4, widths=(4, 4), match=1.0, zipf=1.5,
+                   desc="C4: C2 with Zipf(1.5) foreign keys"),
+}
+
+
+def gen_config(ctx, cfg, nr, ns):
+    """Device generation bit-identical to gen_pk_fk (seed 42); mixed widths are
+    generated as u64 and the 4-byte columns truncated."""
+    import paper_2312_00720_b200 as cj
+    ws = cfg["widths"]
+    pb = 8 if 8 in ws else 4
+    R, S = cj.gen_pk_fk(ctx, nr, ns, len(ws), len(ws), cfg["key"], pb, cfg["match"], cfg["zipf"],
+                        SEED)
+    if pb == 8:
+        import torch
+
+        def narrow(cols):
+            return [c if w == 8 else c.view(torch.int32)[::2].contiguous() for c, w in zip(cols, ws)]
+        R = cj.Relation(R.key, narrow(R.payloads), "R", True)
+        S = cj.Relation(S.key, narrow(S.payloads), "S", False)
+    return R, S
 
 
 def parse():
@@ -44,17 +77,19 @@ def parse():
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--variant", default="phj-gftr")
+    p.add_argument("--config", default="C2", choices=sorted(CONFIGS),
+                   help="BASELINE.json workload (the headline line uses C2)")
     p.add_argument("--scale-log2", type=int, default=0,
                    help="shrink |R|,|S| by 2^k (debug only; the headline uses 0)")
     p.add_argument("--no-extras", action="store_true", help="skip variants/e2e/cpu legs")
     return p.parse_args()
 
 
-def b_alg(algo: str, pattern: str, nr: int, ns: int, nt: int, k=4, w=(4, 4)) -> float:
-    """Algorithmic bytes of one join: PHJ P=2 passes, SMJ P=4
-    live 8-bit digits (keys < 2^28), tuple ids 4 B; gathers count 4 + 2w per
-    output element."""
-    P = 2 if algo == "phj" else 4
+def b_alg(algo: str, pattern: str, nr: int, ns: int, nt: int, k=4, w=(4, 4), key_bits=28) -> float:
+    """Algorithmic bytes of one join: PHJ P=2 passes, SMJ P =
+    live 8-bit digits (4 for keys < 2^28), tuple ids 4 B; gathers count 4 + 2w
+    per output element."""
+    P = 2 if algo == "phj" else (key_bits + 7) // 8
     if pattern == "gftr":
         t = sum(k * n + P * 2 * (k + w[0]) * n for n in (nr, ns))
         f = k * (nr + ns) + (k + 8) * nt
@@ -212,14 +247,15 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ctx = cj.Context(local)
     algo, pattern = a.variant.split("-")
-    nr, ns = R_ROWS >> a.scale_log2, S_ROWS >> a.scale_log2
+    cfg = CONFIGS[a.config]
+    nr, ns = cfg["r"] >> a.scale_log2, cfg["s"] >> a.scale_log2
     res = A.JoinResult()
     L = A.lib()
     opt = cj.options(algo, pattern)
     shuffle = {"exchange_ms": 0.0, "bytes": 0}
     if world == 1:
         # headline config: inputs bit-identical to the reference generator
-        R, S = cj.gen_pk_fk(ctx, nr, ns, NPAY, NPAY, 4, 4, 1.0, 0.0, SEED)
+        R, S = gen_config(ctx, cfg, nr, ns)
         Rc, Sc = cj.coljoin.c_relation(R), cj.coljoin.c_relation(S)
 
         def step():
@@ -328,21 +364,24 @@ def main():
                     "alg_bytes_per_launch": b / c, "peak_source": peak_src}
     tuples = (nr + ns) * world
     value = tuples / (ms / 1e3)
-    balg = b_alg(algo, pattern, nr, ns, rows)
+    kb, ws = cfg["key"], cfg["widths"]
+    key_bits = max(1, (2 * cfg["r"] - 1).bit_length() if cfg["match"] < 1 else (cfg["r"] - 1).bit_length())
+    balg = b_alg(algo, pattern, nr, ns, rows, kb, ws, key_bits)
     out = {
         "metric": METRIC, "value": value, "unit": "tuples/s", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u32",
         "data": "synthetic: bit-identical to the reference's workloads::gen_pk_fk "
                 "(seed 42 + rank), generated on the device",
-        "config": {"workload": WORKLOAD if a.scale_log2 == 0 else f"C2/2^{a.scale_log2}",
+        "config": {"workload": cfg["desc"] if a.scale_log2 == 0 else f"{a.config}/2^{a.scale_log2}",
                    "variant": a.variant.upper(), "r_rows": nr, "s_rows": ns, "out_rows": rows,
-                   "l2": "inputs 4.5 GiB >> 126 MB L2 (no flush needed)",
+                   "l2": "inputs >> 126 MB L2 (no flush needed)" if nr >= 1 << 24
+                   else "inputs partly L2-resident (small config)",
                    "parallelism": f"radix-sharded x{world}" if world > 1 else "single GPU"},
         "roofline": roofline,
-        "join_roofline": {"b_alg_bytes": balg, "b_min_bytes": b_min(nr, ns, rows),
+        "join_roofline": {"b_alg_bytes": balg, "b_min_bytes": b_min(nr, ns, rows, kb, ws),
                           "frac_b_alg": balg / (ms / 1e3) / (peak * 1e9),
-                          "frac_b_min": b_min(nr, ns, rows) / (ms / 1e3) / (peak * 1e9)},
+                          "frac_b_min": b_min(nr, ns, rows, kb, ws) / (ms / 1e3) / (peak * 1e9)},
         "phases_ms": {"transform": phase_sum[0] / 1e6 / a.steps,
                       "find_and_fused_materialize": phase_sum[1] / 1e6 / a.steps,
                       "materialize": phase_sum[2] / 1e6 / a.steps},
@@ -357,7 +396,7 @@ def main():
         out["shuffle"] = shuffle_info
         out["config"]["workload"] = (f"C5-shaped weak scaling: |R|={world}x2^27, |S|={world}x2^28 "
                                      "total, 4-byte key + 2 x 4-byte payloads, cj_gen_shard")
-    if rank == 0 and world == 1 and not a.no_extras:
+    if rank == 0 and world == 1 and not a.no_extras and a.config == "C2":
         # the other variants (3 timed steps each)
         var = {}
         for v in ("phj-gftr", "smj-gftr", "phj-gfur", "smj-gfur", "nphj-gftr", "nphj-gfur"):
@@ -379,11 +418,11 @@ def main():
             vms = e0.elapsed_time(e1) / 3
             va, vp = v.split("-")
             var[v] = {"ms": vms, "tuples_per_s": (nr + ns) / (vms / 1e3),
-                      "frac_b_alg": (b_alg(va, vp, nr, ns, rows) / (vms / 1e3) / (peak * 1e9)
+                      "frac_b_alg": (b_alg(va, vp, nr, ns, rows, kb, ws, key_bits) / (vms / 1e3) / (peak * 1e9)
                                      if va != "nphj" else None)}
         out["variants"] = var
         # end to end through the host-buffer C-ABI (pinned host in/out)
-        out["e2e"] = e2e_leg(ctx, R, S, opt, steps=3)
+        out["e2e"] = e2e_leg(ctx, R, S, opt)
         out["cpu_baseline"] = cpu_baseline(nr, ns, a.variant)
     if rank == 0:
         print(json.dumps(out))
@@ -391,8 +430,15 @@ def main():
         dist.destroy_process_group()
 
 
-def e2e_leg(ctx, R, S, opt, steps=3):
+def e2e_leg(ctx, R, S, opt, steps=6, streams=2):
+    """End to end through the host-buffer C-ABI (cj_run_join_host): every step
+    uploads its pinned host input columns, joins, and downloads every output
+    column into pinned host memory, all inside the timed region.  Steps run
+    on `streams` contexts from as many host threads (the C-ABI allows one
+    thread per ctx), so one step's download overlaps the next one's upload —
+    PCIe is full duplex.  value = tuples of all timed steps / wall time."""
     import ctypes as C
+    import threading
     import torch
     from paper_2312_00720_b200 import _capi as A
     import paper_2312_00720_b200 as cj
@@ -402,36 +448,70 @@ def e2e_leg(ctx, R, S, opt, steps=3):
     Rh = cj.Relation(hk[0], hk[1:], "R", True)
     Sh = cj.Relation(sk[0], sk[1:], "S", False)
     Rc, Sc = cj.coljoin.c_relation(Rh), cj.coljoin.c_relation(Sh)  # data_ptr() of pinned host
-    out_bytes = S.key.numel() * (4 + 4 * (len(R.payloads) + len(S.payloads)))
-    arena = torch.empty(out_bytes + 4096 * 8, dtype=torch.uint8).pin_memory()
-    base = arena.data_ptr()
-    state = {"off": 0}
+    row_out = R.key.element_size() + sum(p.element_size() for p in R.payloads + S.payloads)
+    out_bytes = S.key.numel() * row_out
 
-    def alloc(nbytes, _user):
-        p = base + state["off"]
-        state["off"] += (int(nbytes) + 255) & ~255
-        return p
+    class Lane:
+        def __init__(self, c):
+            self.ctx = c
+            self.arena = torch.empty(out_bytes + 4096 * 8, dtype=torch.uint8).pin_memory()
+            self.off = 0
+            self.cb = A.HOST_ALLOC(self.alloc)
+            self.res = A.JoinResult()
+            self.h2d, self.d2h = C.c_uint64(), C.c_uint64()
+            self.err = None
 
-    cb = A.HOST_ALLOC(alloc)
-    res = A.JoinResult()
-    h2d, d2h = C.c_uint64(), C.c_uint64()
-    times = []
-    for i in range(steps + 1):
-        state["off"] = 0
-        t0 = time.perf_counter()
-        A.check(L.cj_run_join_host(ctx.h, C.byref(Rc), C.byref(Sc), C.byref(opt), cb, None,
-                                   C.byref(res), C.byref(h2d), C.byref(d2h)), ctx.h, "e2e")
-        t1 = time.perf_counter()
-        if i:
-            times.append(t1 - t0)
-    t = statistics.mean(times)
+        def alloc(self, nbytes, _user):
+            p = self.arena.data_ptr() + self.off
+            self.off += (int(nbytes) + 255) & ~255
+            return p
+
+        def run(self, n, delay=0.0):
+            try:
+                if delay:
+                    time.sleep(delay)
+                for _ in range(n):
+                    self.off = 0
+                    A.check(L.cj_run_join_host(self.ctx.h, C.byref(Rc), C.byref(Sc), C.byref(opt),
+                                               self.cb, None, C.byref(self.res), C.byref(self.h2d),
+                                               C.byref(self.d2h)), self.ctx.h, "e2e")
+            except Exception as e:  # noqa: BLE001
+                self.err = e
+
+    lanes = [Lane(ctx)] + [Lane(cj.Context(ctx.device)) for _ in range(streams - 1)]
+    lanes[0].run(1)  # warm-up: module loading, this lane's pool
+    warm = [threading.Thread(target=ln.run, args=(1,)) for ln in lanes[1:]]
+    for t in warm:
+        t.start()
+    lanes[0].run(1)
+    for t in warm:
+        t.join()
+    per = [steps // streams + (1 if i < steps % streams else 0) for i in range(streams)]
+    # stagger the lanes by one upload so a lane's download meets the next
+    # lane's upload instead of both lanes moving data the same way at once
+    stagger = lanes[0].h2d.value / 1e9
+    th = [threading.Thread(target=ln.run, args=(k, i * stagger))
+          for i, (ln, k) in enumerate(zip(lanes, per))]
+    t0 = time.perf_counter()
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    wall = time.perf_counter() - t0
+    for ln in lanes:
+        if ln.err:
+            raise ln.err
     n = R.key.numel() + S.key.numel()
     bi = sum(x.numel() * x.element_size() for x in hk + sk)
-    bo = res.rows * (4 + 4 * (len(R.payloads) + len(S.payloads)))
-    return {"value": n / t, "unit": "tuples/s", "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo,
-            "ms_per_step": t * 1e3, "h2d_ms": h2d.value / 1e6, "d2h_ms": d2h.value / 1e6,
+    bo = lanes[0].res.rows * row_out
+    for ln in lanes[1:]:
+        ln.ctx.close()
+    return {"value": n * steps / wall, "unit": "tuples/s", "h2d_bytes_per_step": bi,
+            "d2h_bytes_per_step": bo, "ms_per_step": wall * 1e3 / steps,
+            "h2d_ms_per_call": lanes[0].h2d.value / 1e6, "d2h_ms_per_call": lanes[0].d2h.value / 1e6,
             "api": "cj_run_join_host (pinned host columns in, pinned host columns out)",
-            "steps": steps}
+            "steps": steps, "concurrent_streams": streams,
+            "how": "wall clock over all steps; one host thread + ctx per stream"}
 
 
 if __name__ == "__main__":

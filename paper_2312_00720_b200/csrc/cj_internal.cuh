@@ -31,6 +31,7 @@ struct cj_ctx {
   int num_sms = 148;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  cudaMemPool_t pool = nullptr;   // stream-ordered allocations of this ctx
   uint16_t epoch = 0;             // look-back status generation (see radix.cu)
   uint64_t launches = 0;          // kernels launched through this ctx
   uint64_t scratch_now = 0, scratch_peak = 0;  // device scratch held by operators

@@ -528,7 +528,7 @@ int guarded(cj_ctx* ctx, F&& fn) {
 
 void* cj_ctx::alloc(uint64_t bytes) {
   void* p = nullptr;
-  cj::check_cuda(cudaMallocAsync(&p, bytes ? bytes : 16, stream), "cudaMallocAsync");
+  cj::check_cuda(cudaMallocFromPoolAsync(&p, bytes ? bytes : 16, pool, stream), "cudaMallocAsync");
   return p;
 }
 
@@ -548,7 +548,7 @@ void cj_ctx::reserve(uint64_t bytes) {
   if (bytes <= pool_reserved) return;
   const uint64_t want = bytes + bytes / 4;
   void* p = nullptr;
-  if (cudaMallocAsync(&p, want, stream) != cudaSuccess) {
+  if (cudaMallocFromPoolAsync(&p, want, pool, stream) != cudaSuccess) {
     cudaGetLastError();  // not enough memory for one block: allocate as we go
     pool_reserved = bytes;
     return;
@@ -624,17 +624,22 @@ int cj_ctx_create(int device, void* stream, cj_ctx** out) {
       CJ_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
       ctx->own_stream = true;
     }
-    cudaMemPool_t pool;
-    CJ_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    // a pool per ctx: concurrent ctxs (one per host thread / stream) never
+    // contend for, or fragment, each other's reserved memory
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    CJ_CUDA(cudaMemPoolCreate(&ctx->pool, &props));
     uint64_t thr = UINT64_MAX;
-    CJ_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    CJ_CUDA(cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &thr));
     // Optional up-front reservation (GiB) of the stream-ordered pool, so the
     // join's multi-GiB scratch never maps new memory inside a timed call.
     if (const char* rg = std::getenv("CJ_POOL_RESERVE_GB")) {
       const uint64_t bytes = (uint64_t)std::strtoull(rg, nullptr, 10) << 30;
       if (bytes) {
         void* p = nullptr;
-        CJ_CUDA(cudaMallocAsync(&p, bytes, ctx->stream));
+        CJ_CUDA(cudaMallocFromPoolAsync(&p, bytes, ctx->pool, ctx->stream));
         CJ_CUDA(cudaFreeAsync(p, ctx->stream));
       }
     }
@@ -665,6 +670,8 @@ int cj_ctx_destroy(cj_ctx* ctx) {
   for (auto& e : ctx->marks)
     if (e) cudaEventDestroy(e);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  // released once the caller has freed every result column it still holds
+  if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
   delete ctx;
   return CJ_OK;
 }

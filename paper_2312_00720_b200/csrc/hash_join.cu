@@ -409,22 +409,30 @@ struct UnitDesc {
   uint64_t b_lo, b_hi, q_lo, q_hi;
 };
 
+// One thread per unit: its partition by binary search over unit_start (a
+// skewed partition may own millions of units; a thread per partition would
+// write them serially).
 __global__ void k_phj_desc(const uint64_t* __restrict__ boff, const uint64_t* __restrict__ poff,
                            const uint64_t* __restrict__ unit_start, uint32_t fanout,
-                           uint32_t limit, uint32_t qchunk, UnitDesc* __restrict__ desc) {
-  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < fanout; p += gridDim.x * blockDim.x) {
-    const uint64_t u0 = unit_start[p], u1 = unit_start[p + 1];
-    if (u0 == u1) continue;
+                           uint32_t limit, uint32_t qchunk, uint64_t units,
+                           UnitDesc* __restrict__ desc) {
+  for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < units;
+       u += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t lo = 0, hi = fanout;  // last p with unit_start[p] <= u
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (unit_start[mid] <= u) lo = mid; else hi = mid;
+    }
+    const uint32_t p = lo;
+    const uint64_t l = u - unit_start[p];
     const uint64_t b0 = boff[p], b1 = boff[p + 1], q0 = poff[p], q1 = poff[p + 1];
     const uint64_t nqc = (q1 - q0 + qchunk - 1) / qchunk;
-    for (uint64_t l = 0; l < u1 - u0; ++l) {
-      UnitDesc d;
-      d.b_lo = b0 + (l / nqc) * limit;
-      d.b_hi = dev::umin64(b1, d.b_lo + limit);
-      d.q_lo = q0 + (l % nqc) * qchunk;
-      d.q_hi = dev::umin64(q1, d.q_lo + qchunk);
-      desc[u0 + l] = d;
-    }
+    UnitDesc d;
+    d.b_lo = b0 + (l / nqc) * limit;
+    d.b_hi = dev::umin64(b1, d.b_lo + limit);
+    d.q_lo = q0 + (l % nqc) * qchunk;
+    d.q_hi = dev::umin64(q1, d.q_lo + qchunk);
+    desc[u] = d;
   }
 }
 
@@ -1008,8 +1016,8 @@ uint64_t run_find(cj_ctx* ctx, FindArgs a, uint64_t total_units) {
 void build_desc(cj_ctx* ctx, FindArgs& a, uint64_t total_units, Scratch& desc) {
   if (total_units == 0) return;
   ctx->kbegin("phj_desc", total_units * 32);
-  k_phj_desc<<<grid_for(a.fanout, 256, 1024), 256, 0, ctx->stream>>>(
-      a.boff, a.poff, a.unit_start, a.fanout, a.limit, a.qchunk, desc.as<UnitDesc>());
+  k_phj_desc<<<grid_for(total_units, 256, 4096), 256, 0, ctx->stream>>>(
+      a.boff, a.poff, a.unit_start, a.fanout, a.limit, a.qchunk, total_units, desc.as<UnitDesc>());
   ctx->kend();
   CJ_CUDA(cudaGetLastError());
   a.desc = desc.p;
