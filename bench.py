@@ -49,7 +49,29 @@ CONFIGS = {
                    desc="C4: C2 with Zipf(1.0) foreign keys"),
     "C4z1.5": dict(r=R_ROWS, s=S_ROWS, key=4, widths=(4, 4), match=1.0, zipf=1.5,
                    desc="C4: C2 with Zipf(1.5) foreign keys"),
+    # configs[4]'s "3-way star join chain" at the paper's sequence shape
+    # (|F|=2^27, |D|=2^25): run_join_sequence, device-resident
+    "STAR3": dict(r=1 << 25, s=1 << 27, key=4, widths=(4,), match=1.0, zipf=0.0, dims=3,
+                  desc="STAR3: run_join_sequence of 3 PK-FK joins, |F|=2^27 fact rows, "
+                       "3 dimensions of 2^25 rows (gen_star, seed 42), one 4-byte payload each"),
 }
+
+
+def b_alg_star(algo, pattern, nf, nd, dims):
+    """Sum over the chain (SURVEY.md §8d formula per join) plus the FK gathers
+    between joins: join i probes (FK_i, ID, P_1..P_{i-1}) — i + 1 payload
+    columns — against a dimension (key + one payload); the probe's columns
+    beyond the first cost what the formula charges any further payload column."""
+    kbits = max(1, (nd - 1).bit_length())
+    P = 2 if algo == "phj" else (kbits + 7) // 8
+    tot = 0.0
+    for i in range(dims):
+        tot += b_alg(algo, pattern, nd, nf, nf, 4, (4,), kbits)
+        per_col = (P * 2 * (4 + 4) + (4 + 2 * 4)) if pattern == "gftr" else (4 + 2 * 4)
+        tot += i * per_col * nf
+        if i + 1 < dims:
+            tot += (4 + 2 * 4) * nf  # FK fetch: map read + gather
+    return float(tot)
 
 
 def gen_config(ctx, cfg, nr, ns):
@@ -255,16 +277,34 @@ def main():
     shuffle = {"exchange_ms": 0.0, "bytes": 0}
     if world == 1:
         # headline config: inputs bit-identical to the reference generator
-        R, S = gen_config(ctx, cfg, nr, ns)
+        if "dims" in cfg:
+            fact, dims = cj.gen_star(ctx, ns, cfg["dims"], nr, SEED)
+            Fc = cj.coljoin.c_relation(fact)
+            Dc = (A.Relation * cfg["dims"])(*[cj.coljoin.c_relation(d) for d in dims])
+            st = (A.SequenceStep * cfg["dims"])()
+            R, S = dims[0], fact
+
+            def step():
+                A.check(L.cj_run_join_sequence(ctx.h, C.byref(Fc), Dc, cfg["dims"], C.byref(opt),
+                                               st, C.byref(res)), ctx.h, "run_join_sequence")
+                rows = res.rows
+                phases = tuple(sum(getattr(st[i], f) for i in range(cfg["dims"]))
+                               for f in ("transform_ns", "find_ns", "materialize_ns"))
+                A.check(L.cj_result_free(ctx.h, C.byref(res)), ctx.h, "free")
+                return rows, phases
+        else:
+            R, S = gen_config(ctx, cfg, nr, ns)
         Rc, Sc = cj.coljoin.c_relation(R), cj.coljoin.c_relation(S)
 
-        def step():
+        def step_join():
             A.check(L.cj_run_join(ctx.h, C.byref(Rc), C.byref(Sc), C.byref(opt), C.byref(res)),
                     ctx.h, "run_join")
             rows = res.rows
             phases = (res.transform_ns, res.find_ns, res.materialize_ns)
             A.check(L.cj_result_free(ctx.h, C.byref(res)), ctx.h, "free")
             return rows, phases
+        if "dims" not in cfg:
+            step = step_join
     else:
         # weak scaling: every rank owns a C2-sized slice of a world-times larger
         # PK-FK join; rows are shuffled to their key's shard over NCCL
@@ -362,11 +402,13 @@ def main():
         roofline = {"bound": "hbm", "kernel": dom["kernel"], "achieved": achieved, "peak": peak,
                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                     "alg_bytes_per_launch": b / c, "peak_source": peak_src}
-    tuples = (nr + ns) * world
+    tuples = (nr + ns) * world * cfg.get("dims", 1)
     value = tuples / (ms / 1e3)
     kb, ws = cfg["key"], cfg["widths"]
     key_bits = max(1, (2 * cfg["r"] - 1).bit_length() if cfg["match"] < 1 else (cfg["r"] - 1).bit_length())
     balg = b_alg(algo, pattern, nr, ns, rows, kb, ws, key_bits)
+    if "dims" in cfg:
+        balg = b_alg_star(algo, pattern, ns, nr, cfg["dims"])
     out = {
         "metric": METRIC, "value": value, "unit": "tuples/s", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",

@@ -218,6 +218,32 @@ int cj_run_join_host(cj_ctx* ctx, const cj_relation* build, const cj_relation* p
                      const cj_join_options* opt, cj_host_alloc_fn alloc, void* user,
                      cj_join_result* res_host, uint64_t* h2d_ns, uint64_t* d2h_ns);
 
+/* ---- chained star joins (sequence.hpp:10-26 run_join_sequence) ----------- */
+typedef struct {                   /* SequenceStep (sequence.hpp:10-15) */
+  uint64_t rows;                   /* output cardinality of this join */
+  uint32_t output_columns;         /* key + carried payloads + dim payload */
+  uint64_t transform_ns, find_ns, materialize_ns;
+  uint64_t fk_fetch_ns;            /* gathering the next FK column, between joins */
+} cj_sequence_step;
+
+/* run_join_sequence(fact, dims, algorithm, pattern, options) — sequence.cpp:9-67,
+ * device-resident: join i probes (FK_i, ID, P_1..P_{i-1}) against dims[i]; the
+ * result's ID column gathers FK_{i+1} on the device (no host copy between the
+ * joins; every intermediate is released as soon as the next probe no longer
+ * needs it).  fact: key = u32 tuple ids, pay[0..n_dims) = FK columns.  steps
+ * receives n_dims entries; last (optional) receives the final join's output
+ * (release with cj_result_free), else it is released. */
+int cj_run_join_sequence(cj_ctx* ctx, const cj_relation* fact, const cj_relation* dims,
+                         uint32_t n_dims, const cj_join_options* opt, cj_sequence_step* steps,
+                         cj_join_result* last);
+
+/* workloads::gen_star (workloads.cpp:135-160), bit-identical: fact_ids u32
+ * iota; fks[d] (key_bytes) FK_d; dim_keys[d] (key_bytes) a Fisher-Yates
+ * permutation of [0, dim_rows); dim_pays[d] (pay_bytes) its payload. */
+int cj_gen_star(cj_ctx* ctx, uint64_t fact_rows, uint32_t dims, uint64_t dim_rows, uint64_t seed,
+                uint32_t key_bytes, uint32_t pay_bytes, void* fact_ids, void* const* fks,
+                void* const* dim_keys, void* const* dim_pays);
+
 /* ---- multi-GPU radix sharding (no reference counterpart) ---- */
 /* Stable partition of a relation's rows by shard s(key) = floor(mix64(key) *
  * parts / 2^64) (mix64 = rng.hpp:8-12), the send layout of the all-to-all

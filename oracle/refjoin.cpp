@@ -7,6 +7,9 @@
 //                 [--reps N] [--warmup W] [--threads T] [--prealloc] [--digest] [--dump DIR]
 //   refjoin prim  --n N --seed S [--dump DIR]
 //   refjoin gen   [workload opts] --dump DIR
+//   refjoin star  --fact N --dims D --dim-rows M --seed S --algo phj|smj --pattern gftr|gfur
+//                 [--reps N] [--threads T]   (workloads::gen_star + the reference's
+//                 run_join_sequence loop, sequence.cpp:9-67, keeping the last output)
 //   (--swap builds on S, whose keys repeat, and probes with R)
 //
 // Workload options mirror workloads::WorkloadSpec (workloads.hpp:11-21):
@@ -35,6 +38,7 @@
 #include "coljoin/primitives.hpp"
 #include "coljoin/reference.hpp"
 #include "coljoin/rng.hpp"
+#include "coljoin/sequence.hpp"
 #include "coljoin/workloads.hpp"
 
 using namespace coljoin;
@@ -216,6 +220,82 @@ int cmd_gen(const Args& a) {
   return 0;
 }
 
+// Star schema (workloads.cpp:135-160) and the chained joins of
+// run_join_sequence (sequence.cpp:9-67).  The reference's function returns the
+// steps only; the loop is restated here with the reference's own run_join and
+// gather_copy so that the final join's output can be digested, and the
+// reference's run_join_sequence is timed as is (--reps).
+int cmd_star(const Args& a) {
+  workloads::StarSchemaSpec spec;
+  spec.fact_rows = std::strtoull(a.get("--fact", "4096"), nullptr, 10);
+  spec.dims = static_cast<unsigned>(std::atoi(a.get("--dims", "3")));
+  spec.dim_rows = std::strtoull(a.get("--dim-rows", "1024"), nullptr, 10);
+  spec.seed = std::strtoull(a.get("--seed", "42"), nullptr, 10);
+  auto star = workloads::gen_star(spec);
+  JoinTask proto;
+  proto.algorithm = std::strcmp(a.get("--algo", "phj"), "smj") == 0 ? JoinAlgo::SMJ : JoinAlgo::PHJ;
+  proto.pattern = std::strcmp(a.get("--pattern", "gftr"), "gfur") == 0 ? JoinPattern::GFUR
+                                                                       : JoinPattern::GFTR;
+  proto.options.worker_count = static_cast<unsigned>(std::atoi(a.get("--threads", "0")));
+  proto.options.preallocate = a.has("--prealloc");
+  const unsigned workers = proto.options.worker_count ? proto.options.worker_count
+                                                      : static_cast<unsigned>(omp_get_max_threads());
+  std::printf("{\"fact_ids\": \"%016llx\"", (unsigned long long)digest_col(star.fact.key));
+  for (size_t d = 0; d < star.dims.size(); ++d)
+    std::printf(", \"fk%zu\": \"%016llx\", \"dim%zu_key\": \"%016llx\", \"dim%zu_p0\": \"%016llx\"", d,
+                (unsigned long long)digest_col(star.fact.payloads[d]), d,
+                (unsigned long long)digest_col(star.dims[d].key), d,
+                (unsigned long long)digest_col(star.dims[d].payloads[0]));
+  // the chain, as sequence.cpp:23-66
+  Relation probe;
+  probe.key = star.fact.payloads[0];
+  probe.payloads.push_back(star.fact.key);
+  std::printf(", \"steps\": [");
+  for (size_t i = 0; i < star.dims.size(); ++i) {
+    JoinTask task = proto;
+    task.build = &star.dims[i];
+    task.probe = &probe;
+    JoinOutput out = run_join(task);
+    std::vector<uint64_t> flat = widen(out.relation.key);
+    for (const auto& c : out.relation.payloads) {
+      auto w = widen(c);
+      flat.insert(flat.end(), w.begin(), w.end());
+    }
+    std::printf("%s{\"rows\": %zu, \"columns\": %zu, \"digest\": \"%016llx\", \"order_digest\": \"%016llx\"}",
+                i ? ", " : "", out.relation.rows(), out.relation.column_count(),
+                (unsigned long long)digest_words(oracle::canonical_rows(out.relation)),
+                (unsigned long long)digest_words(flat));
+    if (i + 1 < star.dims.size()) {
+      const size_t dim_pay = star.dims[i].payloads.size();
+      Column next_fk =
+          primitives::gather_copy(star.fact.payloads[i + 1], out.relation.payloads[dim_pay].u32(), workers);
+      probe = Relation{};
+      probe.key = std::move(next_fk);
+      for (size_t c = dim_pay; c < out.relation.payloads.size(); ++c)
+        probe.payloads.push_back(std::move(out.relation.payloads[c]));
+      for (size_t c = 0; c < dim_pay; ++c) probe.payloads.push_back(std::move(out.relation.payloads[c]));
+    }
+  }
+  std::printf("]");
+  const int reps = std::atoi(a.get("--reps", "0"));
+  if (reps > 0) {
+    std::vector<uint64_t> t;
+    for (int r = 0; r < reps; ++r) {
+      const auto t0 = std::chrono::steady_clock::now();
+      auto steps = run_join_sequence(star.fact, star.dims, proto.algorithm, proto.pattern,
+                                     proto.options);
+      t.push_back(static_cast<uint64_t>(std::chrono::duration_cast<std::chrono::nanoseconds>(
+                                            std::chrono::steady_clock::now() - t0)
+                                            .count()));
+    }
+    std::sort(t.begin(), t.end());
+    std::printf(", \"sequence_ns_median\": %llu, \"threads\": %u", (unsigned long long)t[t.size() / 2],
+                workers);
+  }
+  std::printf("}\n");
+  return 0;
+}
+
 // Primitive known-answer digests on seeded inputs (for pinning the C port).
 // Inputs: keys_i = CounterRng(seed).at(i) truncated/bounded as noted.
 int cmd_prim(const Args& a) {
@@ -318,6 +398,7 @@ int main(int argc, char** argv) {
     if (std::strcmp(argv[1], "join") == 0) return cmd_join(a);
     if (std::strcmp(argv[1], "gen") == 0) return cmd_gen(a);
     if (std::strcmp(argv[1], "prim") == 0) return cmd_prim(a);
+    if (std::strcmp(argv[1], "star") == 0) return cmd_star(a);
   } catch (const std::exception& e) {
     std::fprintf(stderr, "refjoin: %s\n", e.what());
     return 1;

@@ -75,6 +75,12 @@ class JoinResult(C.Structure):
                 ("device_bytes_peak", C.c_uint64)]
 
 
+class SequenceStep(C.Structure):
+    _fields_ = [("rows", C.c_uint64), ("output_columns", C.c_uint32),
+                ("transform_ns", C.c_uint64), ("find_ns", C.c_uint64),
+                ("materialize_ns", C.c_uint64), ("fk_fetch_ns", C.c_uint64)]
+
+
 class Partitioned(C.Structure):
     _fields_ = [("keys", C.c_void_p), ("offsets", C.c_void_p), ("carried", C.c_void_p),
                 ("rows", C.c_uint64)]
@@ -131,6 +137,11 @@ PROTOS = {
     "cj_scratch_peak": (C.c_uint64, [_P, C.c_int]),
     "cj_gen_pk_fk": (C.c_int, [_P, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
                                C.c_uint32, C.c_double, C.c_double, C.c_uint64, _P, _PP, _P, _PP]),
+    "cj_run_join_sequence": (C.c_int, [_P, C.POINTER(Relation), C.POINTER(Relation), C.c_uint32,
+                                       C.POINTER(JoinOptions), C.POINTER(SequenceStep),
+                                       C.POINTER(JoinResult)]),
+    "cj_gen_star": (C.c_int, [_P, C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint32,
+                              C.c_uint32, _P, _PP, _PP, _PP]),
 }
 
 _lib = None

@@ -429,3 +429,53 @@ def gen_pk_fk(ctx: Context, r_rows, s_rows, r_payloads=1, s_payloads=1, key_byte
                                pay_bytes, match_ratio, zipf_factor, seed, rk.data_ptr(),
                                _ptrs(rp), sk.data_ptr(), _ptrs(sp)), ctx.h, "gen_pk_fk")
     return (Relation(rk, rp, "R", True), Relation(sk, sp, "S", False))
+
+
+@dataclass
+class SequenceStep:
+    """sequence.hpp:10-15."""
+    rows: int
+    output_columns: int
+    report: PhaseReport
+    fk_fetch_ns: int
+
+
+def run_join_sequence(ctx: Context, fact: Relation, dims: Sequence, algo="phj", pattern="gftr",
+                      **kw):
+    """sequence.hpp:21-24 run_join_sequence, device-resident (no host copy
+    between the joins).  Returns (steps, final JoinOutput)."""
+    opt = options(algo, pattern, **kw)
+    F = c_relation(fact)
+    D = (A.Relation * max(len(dims), 1))(*[c_relation(d) for d in dims])
+    st = (A.SequenceStep * max(len(dims), 1))()
+    res = A.JoinResult()
+    check(A.lib().cj_run_join_sequence(ctx.h, C.byref(F), D, len(dims), C.byref(opt), st,
+                                       C.byref(res)), ctx.h, "run_join_sequence")
+    steps = [SequenceStep(st[i].rows, st[i].output_columns,
+                          PhaseReport(st[i].transform_ns, st[i].find_ns, st[i].materialize_ns),
+                          st[i].fk_fetch_ns) for i in range(len(dims))]
+    if not dims:
+        return steps, None
+    t = res.rows
+    last = dims[-1]
+    nr = len(last.payloads)
+    key = _wrap(ctx, res.key, t, _nbytes(last.key))
+    pays = [_wrap(ctx, res.pay[i], t, _nbytes(last.payloads[i])) for i in range(nr)]
+    # carried probe columns: (ID, payloads of dims 1..n-1)  (sequence.cpp:56-62)
+    widths = [4] + [_nbytes(p) for d in dims[:-1] for p in d.payloads]
+    pays += [_wrap(ctx, res.pay[nr + i], t, w) for i, w in enumerate(widths)]
+    return steps, JoinOutput(Relation(key, pays, "sequence"),
+                             PhaseReport(res.transform_ns, res.find_ns, res.materialize_ns), t)
+
+
+def gen_star(ctx: Context, fact_rows: int, dims: int, dim_rows: int, seed: int = 0,
+             key_bytes: int = 4, pay_bytes: int = 4):
+    """workloads.hpp:47-61 gen_star, bit-identical, on the device."""
+    ids = _empty(fact_rows, 4)
+    fks = [_empty(fact_rows, key_bytes) for _ in range(dims)]
+    dk = [_empty(dim_rows, key_bytes) for _ in range(dims)]
+    dp = [_empty(dim_rows, pay_bytes) for _ in range(dims)]
+    check(A.lib().cj_gen_star(ctx.h, fact_rows, dims, dim_rows, seed, key_bytes, pay_bytes,
+                              ids.data_ptr(), _ptrs(fks), _ptrs(dk), _ptrs(dp)), ctx.h, "gen_star")
+    fact = Relation(ids, fks, "fact", True)
+    return fact, [Relation(dk[d], [dp[d]], f"dim{d + 1}", True) for d in range(dims)]

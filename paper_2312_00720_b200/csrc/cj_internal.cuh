@@ -223,6 +223,10 @@ void gen_pk_fk(cj_ctx* ctx, uint64_t r_rows, uint64_t s_rows, uint32_t r_pay, ui
 // Exclusive scan of n u64 counts on the ctx stream; *total_dev = sum.
 void scan_counts(cj_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* out, uint64_t* total_dev);
 
+void gen_star(cj_ctx* ctx, uint64_t fact_rows, uint32_t dims, uint64_t dim_rows, uint64_t seed,
+              uint32_t key_bytes, uint32_t pay_bytes, void* fact_ids, void* const* fks,
+              void* const* dim_keys, void* const* dim_pays);
+
 void gen_shard(cj_ctx* ctx, uint64_t r_total, uint64_t s_total, uint32_t rank, uint32_t ranks,
                uint32_t r_pay, uint32_t s_pay, uint64_t seed, void* r_key, void* const* r_pays,
                void* s_key, void* const* s_pays);

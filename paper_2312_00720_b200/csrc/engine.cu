@@ -962,6 +962,118 @@ int cj_run_join(cj_ctx* ctx, const cj_relation* build, const cj_relation* probe,
   });
 }
 
+int cj_run_join_sequence(cj_ctx* ctx, const cj_relation* fact, const cj_relation* dims,
+                         uint32_t n_dims, const cj_join_options* opt, cj_sequence_step* steps,
+                         cj_join_result* last) {
+  return cj::guarded(ctx, [&] {
+    if (!fact || !dims || !opt || !steps) cj::fail(CJ_ERR_SPEC_INVALID, "null argument");
+    if (n_dims == 0) return;
+    if (fact->npay < n_dims) cj::fail(CJ_ERR_SPEC_INVALID, "fact table needs one FK column per dimension");
+    if (fact->key_bytes != 4) cj::fail(CJ_ERR_SPEC_INVALID, "fact tuple ids must be a 4-byte column");
+    // buffers the chain owns (intermediate outputs), released when unused
+    std::vector<void*> owned;
+    auto release = [&](void* p) {
+      for (auto& q : owned)
+        if (q == p) {
+          ctx->release(p);
+          q = nullptr;
+        }
+    };
+    struct Guard {
+      cj_ctx* c;
+      std::vector<void*>* v;
+      ~Guard() {
+        for (void* p : *v)
+          if (p) c->release(p);
+      }
+    } guard{ctx, &owned};
+    // probe for join 1: (FK_1, ID)  (sequence.cpp:23-27)
+    cj_relation probe{};
+    probe.key = fact->pay[0];
+    probe.key_bytes = fact->pay_bytes[0];
+    probe.rows = fact->rows;
+    probe.npay = 1;
+    probe.pay[0] = fact->key;
+    probe.pay_bytes[0] = 4;
+    probe.key_unique = 0;
+    cudaEvent_t e0, e1;
+    CJ_CUDA(cudaEventCreate(&e0));
+    CJ_CUDA(cudaEventCreate(&e1));
+    for (uint32_t i = 0; i < n_dims; ++i) {
+      cj_join_result res{};
+      cj::run_join_dev(ctx, &dims[i], &probe, opt, &res);
+      cj_sequence_step& st = steps[i];
+      st.rows = res.rows;
+      st.output_columns = 1 + dims[i].npay + probe.npay;
+      st.transform_ns = res.transform_ns;
+      st.find_ns = res.find_ns;
+      st.materialize_ns = res.materialize_ns;
+      st.fk_fetch_ns = 0;
+      // the probe's own columns (this chain's, not the caller's) are consumed
+      if (i > 0) {
+        release(const_cast<void*>(probe.key));
+        for (uint32_t c = 0; c < probe.npay; ++c) release(const_cast<void*>(probe.pay[c]));
+      }
+      if (i + 1 == n_dims) {
+        if (last) *last = res;
+        else cj::free_output(ctx, &res);
+        break;
+      }
+      // output payloads are build-side first: (P_i, ID, P_1..P_{i-1}); the
+      // next probe is (FK_{i+1}, ID, P_1..P_i)  (sequence.cpp:38-62)
+      const uint32_t dim_pay = dims[i].npay;
+      const uint32_t* ids = static_cast<const uint32_t*>(res.pay[dim_pay]);
+      void* next_fk = ctx->alloc(std::max<uint64_t>(res.rows * fact->pay_bytes[i + 1], 16) + cj::kPad);
+      owned.push_back(next_fk);
+      CJ_CUDA(cudaEventRecord(e0, ctx->stream));
+      const void* in[1] = {fact->pay[i + 1]};
+      void* out[1] = {next_fk};
+      const uint32_t by[1] = {fact->pay_bytes[i + 1]};
+      cj::gather_cols(ctx, in, fact->rows, ids, res.rows, out, by, 1);
+      CJ_CUDA(cudaEventRecord(e1, ctx->stream));
+      CJ_CUDA(cudaEventSynchronize(e1));
+      float ms = 0;
+      CJ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      st.fk_fetch_ns = static_cast<uint64_t>(ms * 1e6);
+      cj::raise_device_errors(ctx);
+      cj_relation np{};
+      np.key = next_fk;
+      np.key_bytes = fact->pay_bytes[i + 1];
+      np.rows = res.rows;
+      np.key_unique = 0;
+      const uint32_t total_pay = dims[i].npay + probe.npay;
+      if (total_pay > CJ_MAX_COLS) cj::fail(CJ_ERR_UNSUPPORTED, "too many carried payload columns");
+      uint32_t k = 0;
+      for (uint32_t c = dim_pay; c < total_pay; ++c, ++k) {
+        np.pay[k] = res.pay[c];
+        np.pay_bytes[k] = c - dim_pay < probe.npay ? probe.pay_bytes[c - dim_pay] : 4;
+        owned.push_back(res.pay[c]);
+      }
+      for (uint32_t c = 0; c < dim_pay; ++c, ++k) {
+        np.pay[k] = res.pay[c];
+        np.pay_bytes[k] = dims[i].pay_bytes[c];
+        owned.push_back(res.pay[c]);
+      }
+      np.npay = k;
+      ctx->release(res.key);  // the FK key column of the output is not carried
+      if (res.ids_r) ctx->release(res.ids_r);
+      if (res.ids_s) ctx->release(res.ids_s);
+      probe = np;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  });
+}
+
+int cj_gen_star(cj_ctx* ctx, uint64_t fact_rows, uint32_t dims, uint64_t dim_rows, uint64_t seed,
+                uint32_t key_bytes, uint32_t pay_bytes, void* fact_ids, void* const* fks,
+                void* const* dim_keys, void* const* dim_pays) {
+  return cj::guarded(ctx, [&] {
+    cj::gen_star(ctx, fact_rows, dims, dim_rows, seed, key_bytes, pay_bytes, fact_ids, fks,
+                 dim_keys, dim_pays);
+  });
+}
+
 int cj_result_free(cj_ctx* ctx, cj_join_result* res) {
   return cj::guarded(ctx, [&] { cj::free_output(ctx, res); });
 }

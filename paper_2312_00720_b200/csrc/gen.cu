@@ -88,6 +88,27 @@ __global__ void k_payload(uint64_t seed, uint64_t n, T* out) {
     out[i] = (T)rng_at(seed, i);
 }
 
+// workloads.cpp:141-145: fact FK i = stream.below(i, dim_rows)
+template <class K>
+__global__ void k_star_fk(uint64_t seed, uint64_t n, uint64_t bound, K* out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = (K)__umul64hi(rng_at(seed, i), bound);
+}
+
+__global__ void k_iota32(uint32_t* out, uint64_t n) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = (uint32_t)i;
+}
+
+template <class K>
+__global__ void k_perm_keys(const uint32_t* __restrict__ perm, uint64_t n, K* out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = (K)perm[i];
+}
+
 // Bijection of [0, 2^m): rounds of (odd multiply, add, xor-shift), all mod 2^m.
 __device__ __forceinline__ uint64_t scramble(uint64_t x, uint32_t m, uint64_t seed) {
   const uint64_t mask = m >= 64 ? ~0ull : ((1ull << m) - 1);
@@ -236,6 +257,63 @@ void gen_pk_fk(cj_ctx* ctx, uint64_t r_rows, uint64_t s_rows, uint32_t r_pay, ui
   };
   for (uint32_t c = 0; c < r_pay; ++c) pay(r_pays[c], r_rows, 0x7000ull + c);
   for (uint32_t c = 0; c < s_pay; ++c) pay(s_pays[c], s_rows, 0x8000ull + c);
+  CJ_CUDA(cudaGetLastError());
+  CJ_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+// workloads::gen_star (workloads.cpp:135-160): fact key = physical tuple ids
+// (u32 iota), FK_d = stream(0x46b00000 + d).below(i, dim_rows); dimension d =
+// Fisher-Yates permutation of [0, dim_rows) (stream 0xd1a00000 + d, host) as
+// keys + one payload column (stream 0xd1a08000 + d).
+void gen_star(cj_ctx* ctx, uint64_t fact_rows, uint32_t dims, uint64_t dim_rows, uint64_t seed,
+              uint32_t key_bytes, uint32_t pay_bytes, void* fact_ids, void* const* fks,
+              void* const* dim_keys, void* const* dim_pays) {
+  if (dims < 1) fail(CJ_ERR_SPEC_INVALID, "star schema needs at least one dimension");
+  if (dim_rows == 0) fail(CJ_ERR_SPEC_INVALID, "dimension tables cannot be empty");
+  if (fact_rows > 0x7fffffffull || dim_rows > 0x7fffffffull)
+    fail(CJ_ERR_SPEC_INVALID, "row count exceeds the 2^31-1 cap");
+  if ((key_bytes != 4 && key_bytes != 8) || (pay_bytes != 4 && pay_bytes != 8))
+    fail(CJ_ERR_KIND, "key/payload widths must be 4 or 8 bytes");
+  const unsigned grid = ctx->num_sms * 8;
+  if (fact_rows) {
+    ctx->kbegin("gen_star_ids", fact_rows * 4);
+    k_iota32<<<grid, 256, 0, ctx->stream>>>(static_cast<uint32_t*>(fact_ids), fact_rows);
+    ctx->kend();
+  }
+  for (uint32_t d = 0; d < dims; ++d) {
+    if (fact_rows) {
+      const uint64_t fs = stream_of(seed, 0x46b00000ull + d);
+      ctx->kbegin("gen_star_fk", fact_rows * key_bytes);
+      if (key_bytes == 4)
+        k_star_fk<uint32_t><<<grid, 256, 0, ctx->stream>>>(fs, fact_rows, dim_rows,
+                                                           static_cast<uint32_t*>(fks[d]));
+      else
+        k_star_fk<uint64_t><<<grid, 256, 0, ctx->stream>>>(fs, fact_rows, dim_rows,
+                                                           static_cast<uint64_t*>(fks[d]));
+      ctx->kend();
+    }
+    const std::vector<uint32_t> perm = permutation(dim_rows, stream_of(seed, 0xd1a00000ull + d));
+    {
+      Scratch dperm(ctx, dim_rows * 4);
+      CJ_CUDA(cudaMemcpyAsync(dperm.p, perm.data(), dim_rows * 4, cudaMemcpyHostToDevice, ctx->stream));
+      ctx->kbegin("gen_star_dim", dim_rows * (4 + key_bytes));
+      if (key_bytes == 4)
+        k_perm_keys<uint32_t><<<grid, 256, 0, ctx->stream>>>(dperm.as<uint32_t>(), dim_rows,
+                                                             static_cast<uint32_t*>(dim_keys[d]));
+      else
+        k_perm_keys<uint64_t><<<grid, 256, 0, ctx->stream>>>(dperm.as<uint32_t>(), dim_rows,
+                                                             static_cast<uint64_t*>(dim_keys[d]));
+      ctx->kend();
+      CJ_CUDA(cudaStreamSynchronize(ctx->stream));  // perm host buffer lifetime
+    }
+    const uint64_t ps = stream_of(seed, 0xd1a08000ull + d);
+    ctx->kbegin("gen_payload", dim_rows * pay_bytes);
+    if (pay_bytes == 4)
+      k_payload<uint32_t><<<grid, 256, 0, ctx->stream>>>(ps, dim_rows, static_cast<uint32_t*>(dim_pays[d]));
+    else
+      k_payload<uint64_t><<<grid, 256, 0, ctx->stream>>>(ps, dim_rows, static_cast<uint64_t*>(dim_pays[d]));
+    ctx->kend();
+  }
   CJ_CUDA(cudaGetLastError());
   CJ_CUDA(cudaStreamSynchronize(ctx->stream));
 }

@@ -19,6 +19,7 @@
 #include "cj_api.h"
 #include "coljoin/hash_match.hpp"
 #include "coljoin/join_engine.hpp"
+#include "coljoin/sequence.hpp"
 #include "coljoin/merge_match.hpp"
 #include "coljoin/primitives.hpp"
 
@@ -742,6 +743,53 @@ JoinOutput run_join(const JoinTask& task) {
   out.stats.clusteredness_r = res.clusteredness_r;
   out.stats.clusteredness_s = res.clusteredness_s;
   return out;
+}
+
+std::vector<SequenceStep> run_join_sequence(const Relation& fact, const std::vector<Relation>& dims,
+                                            JoinAlgo algorithm, JoinPattern pattern,
+                                            const JoinOptions& options) {
+  const size_t n_joins = dims.size();
+  if (fact.payloads.size() < n_joins)  // sequence.cpp:14-17
+    throw SpecInvalid("fact table needs one FK column per dimension");
+  if (fact.key.kind() != ValueKind::u32) throw SpecInvalid("fact tuple ids must be a 4-byte column");
+  if (options.radix_bits_per_pass == 0 || options.radix_bits_per_pass > 8)
+    throw FanoutTooLarge("radix bits per pass must be in [1, 8]");
+  std::vector<SequenceStep> steps(n_joins);
+  if (n_joins == 0) return steps;
+  for (const auto& dm : dims)
+    if (dm.key.kind() != fact.payloads[0].kind()) throw KindError("build and probe key kinds differ");
+  auto& d = Device::get();
+  std::lock_guard<std::mutex> lock(d.mu());
+  std::vector<Buf> fc = upload_relation(fact);
+  cj_relation F = describe(fact, fc);
+  std::vector<std::vector<Buf>> dc;
+  std::vector<cj_relation> D;
+  dc.reserve(n_joins);
+  for (const auto& dm : dims) {
+    dc.push_back(upload_relation(dm));
+    D.push_back(describe(dm, dc.back()));
+  }
+  cj_join_options opt;
+  cj_default_options(&opt);
+  opt.algo = static_cast<int>(algorithm);
+  opt.pattern = static_cast<int>(pattern);
+  opt.radix_bits_per_pass = options.radix_bits_per_pass;
+  opt.total_radix_bits = options.total_radix_bits;
+  opt.sub_partition_limit = options.sub_partition_limit;
+  opt.validate = options.validate ? 1 : 0;
+  std::vector<cj_sequence_step> st(n_joins);
+  d.check(cj_run_join_sequence(d.ctx(), &F, D.data(), static_cast<uint32_t>(n_joins), &opt,
+                               st.data(), nullptr),
+          "run_join_sequence");
+  for (size_t i = 0; i < n_joins; ++i) {
+    steps[i].rows = st[i].rows;
+    steps[i].output_columns = st[i].output_columns;
+    steps[i].report.transform_ns = st[i].transform_ns;
+    steps[i].report.find_ns = st[i].find_ns;
+    steps[i].report.materialize_ns = st[i].materialize_ns;
+    steps[i].fk_fetch_ns = st[i].fk_fetch_ns;
+  }
+  return steps;
 }
 
 Relation make_join_output_shell(const MatchSet& match, const Relation& r, const Relation& s) {

@@ -13,6 +13,7 @@ Only runs where /root/reference exists (this container); the JSON is committed.
 
     python tests/golden/make_golden.py            # everything
     python tests/golden/make_golden.py --c2-gen   # append the C2 generator digests only
+    python tests/golden/make_golden.py --star     # (re)write the star-chain cells only
 """
 import json
 import os
@@ -63,10 +64,39 @@ def add_c2_gen():
         json.dump(out, f, indent=1, sort_keys=True)
 
 
+STAR_CELLS = [dict(fact=4096, dims=3, dim_rows=1024, seed=42),
+              dict(fact=1 << 18, dims=4, dim_rows=1 << 16, seed=44),
+              dict(fact=1 << 20, dims=3, dim_rows=1 << 18, seed=42)]
+STAR3 = dict(fact=1 << 27, dims=3, dim_rows=1 << 25, seed=42, name="STAR3")
+
+
+def add_star():
+    """workloads::gen_star + the chained joins (refjoin star): column digests of
+    the inputs and, per join, rows / columns / canonical and emission digests."""
+    path = os.path.join(HERE, "golden.json")
+    with open(path) as f:
+        out = json.load(f)
+    out["star"] = []
+    cells = STAR_CELLS + ([STAR3] if os.environ.get("GOLDEN_STAR3") else [])
+    for c in cells:
+        for algo, pat in (("phj", "gftr"), ("smj", "gfur"), ("phj", "gfur"), ("smj", "gftr")):
+            if c.get("name") == "STAR3" and (algo, pat) != ("phj", "gftr"):
+                continue
+            r = O.refjoin("star", "--fact", str(c["fact"]), "--dims", str(c["dims"]), "--dim-rows",
+                          str(c["dim_rows"]), "--seed", str(c["seed"]), "--algo", algo, "--pattern",
+                          pat, "--threads", "8")
+            out["star"].append(dict(cell=c, algo=algo, pattern=pat, ref=r))
+            print(c, algo, pat, file=sys.stderr)
+    with open(path, "w") as f:
+        json.dump(out, f, indent=1, sort_keys=True)
+
+
 def main():
     O.build()
     if "--c2-gen" in sys.argv:
         return add_c2_gen()
+    if "--star" in sys.argv:
+        return add_star()
     out = {"join": [], "gen": [], "prim": {}}
     cells = grid()
     cells.append(dict(r=1 << 20, s=1 << 22, match=1.0, zipf=0.0, key="u32", pay="u32", rpay=1,
