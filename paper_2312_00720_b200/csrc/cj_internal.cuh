@@ -213,7 +213,8 @@ void check_sorted(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes, bool
 
 // nphj.cu: non-partitioned (global table) hash join.
 uint64_t nphj_find(cj_ctx* ctx, const void* rkeys, uint64_t nr, const void* skeys, uint64_t ns,
-                   int key_bytes, const OutSpec& out, uint64_t capacity, bool count_only);
+                   int key_bytes, const OutSpec& out, uint64_t capacity, bool count_only,
+                   bool unique = false);
 
 // gen.cu
 void gen_pk_fk(cj_ctx* ctx, uint64_t r_rows, uint64_t s_rows, uint32_t r_pay, uint32_t s_pay,

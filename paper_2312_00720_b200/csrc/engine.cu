@@ -341,7 +341,7 @@ void run_join_dev(cj_ctx* ctx, const cj_relation* R, const cj_relation* S,
     }
     uint64_t total;
     try {
-      total = nphj_find(ctx, R->key, R->rows, S->key, S->rows, kb, o, cap, false);
+      total = nphj_find(ctx, R->key, R->rows, S->key, S->rows, kb, o, cap, false, pk_fk);
     } catch (const Error& e) {
       if (e.code != CJ_ERR_CAPACITY_EXCEEDED || !pk_fk) throw;
       free_output(ctx, res);

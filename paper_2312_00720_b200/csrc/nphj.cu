@@ -49,6 +49,7 @@ struct NphjArgs {
   uint64_t capacity;
   int write;
   uint64_t* total_out;
+  int unique;                // build keys unique (Relation::key_unique): one match per probe
 };
 
 template <class K>
@@ -76,22 +77,155 @@ __global__ void __launch_bounds__(kThreads) k_nphj_build(const __grid_constant__
     while (true) {
       uint32_t* s = a.table + h * a.slot_words;
       if (atomicCAS(s, 0u, (uint32_t)(i + 1)) == 0u) {
-        s[1] = (uint32_t)k;
-        if constexpr (sizeof(K) == 8) s[2] = (uint32_t)((uint64_t)k >> 32);
-        for (int c = 0; c < a.nr_cols; ++c) {
-          uint32_t* d = s + a.r_word_off[c];
-          if (a.r_bytes[c] == 4) {
-            d[0] = static_cast<const uint32_t*>(a.r_src[c])[i];
+        if (a.slot_words == 4 && sizeof(K) == 4) {
+          // one 16-byte store of the whole slot (word 0 rewritten with its own value)
+          uint32_t w2 = 0, w3 = 0;
+          if (a.nr_cols == 1 && a.r_bytes[0] == 8) {
+            const uint64_t v = static_cast<const uint64_t*>(a.r_src[0])[i];
+            w2 = (uint32_t)v;
+            w3 = (uint32_t)(v >> 32);
           } else {
-            const uint64_t v = static_cast<const uint64_t*>(a.r_src[c])[i];
-            d[0] = (uint32_t)v;
-            d[1] = (uint32_t)(v >> 32);
+            if (a.nr_cols > 0) w2 = static_cast<const uint32_t*>(a.r_src[0])[i];
+            if (a.nr_cols > 1) w3 = static_cast<const uint32_t*>(a.r_src[1])[i];
+          }
+          *reinterpret_cast<uint4*>(s) = make_uint4((uint32_t)(i + 1), (uint32_t)k, w2, w3);
+        } else {
+          s[1] = (uint32_t)k;
+          if constexpr (sizeof(K) == 8) s[2] = (uint32_t)((uint64_t)k >> 32);
+          for (int c = 0; c < a.nr_cols; ++c) {
+            uint32_t* d = s + a.r_word_off[c];
+            if (a.r_bytes[c] == 4) {
+              d[0] = static_cast<const uint32_t*>(a.r_src[c])[i];
+            } else {
+              const uint64_t v = static_cast<const uint64_t*>(a.r_src[c])[i];
+              d[0] = (uint32_t)v;
+              d[1] = (uint32_t)(v >> 32);
+            }
           }
         }
         break;
       }
       h = (h + 1) & mask;
     }
+  }
+}
+
+// Unique build keys (Relation::key_unique, as the reference's PK-FK merge
+// trusts it, merge_match.cpp:65-68): a probe stops at its first match; a
+// 4-word slot (4-byte key + <= 8 payload bytes) is read with one 16-byte load
+// and its payload words are kept in shared memory for the write, so the table
+// is touched once per probe step.
+template <class K, bool VEC>
+__global__ void __launch_bounds__(kThreads) k_nphj_probe_u(const __grid_constant__ NphjArgs a) {
+  __shared__ uint32_t s_hit[kTile];      // 0: no match, else build row + 1
+  __shared__ uint2 s_pay[VEC ? kTile : 1];  // slot words 2, 3 of the match
+  __shared__ uint64_t s_t, s_base;
+  __shared__ uint64_t s_wcount[kWarps], s_wbase[kWarps];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const K* __restrict__ sk = static_cast<const K*>(a.skeys);
+  const uint64_t mask = (1ull << a.log2cap) - 1;
+  while (true) {
+    if (tid == 0) s_t = atomicAdd(a.ticket, 1u);
+    __syncthreads();
+    const uint64_t t = s_t;
+    if (t >= a.tiles) break;
+    const uint64_t j0 = t * kTile;
+    const uint32_t nq = (uint32_t)dev::umin64(kTile, a.ns - j0);
+    const uint32_t rounds = (nq + 31) / 32;
+    const uint32_t r0 = rounds * warp / kWarps, r1 = rounds * (warp + 1) / kWarps;
+    uint64_t wc = 0;
+    for (uint32_t rr = r0; rr < r1; ++rr) {
+      const uint32_t jl = rr * 32 + lane;
+      uint32_t hit = 0;
+      if (jl < nq) {
+        const K k = __ldcs(sk + j0 + jl);
+        uint64_t h = nslot(k, a.log2cap);
+        while (true) {
+          const uint32_t* s = a.table + h * a.slot_words;
+          if (VEC) {
+            const uint4 w = __ldg(reinterpret_cast<const uint4*>(s));
+            if (w.x == 0) break;
+            if (w.y == (uint32_t)k) {
+              hit = w.x;
+              s_pay[jl] = make_uint2(w.z, w.w);
+              break;
+            }
+          } else {
+            const uint32_t row1 = s[0];
+            if (row1 == 0) break;
+            if (slot_key<K>(s) == k) {
+              hit = row1;
+              break;
+            }
+          }
+          h = (h + 1) & mask;
+        }
+        s_hit[jl] = hit;
+      }
+      wc += __popc(__ballot_sync(0xffffffffu, hit != 0));
+    }
+    if (lane == 0) s_wcount[warp] = wc;
+    __syncthreads();
+    if (warp == 0) {
+      const uint64_t v = lane < kWarps ? s_wcount[lane] : 0;
+      const uint64_t inc = dev::warp_inclusive_sum(v);
+      if (lane < kWarps) s_wbase[lane] = inc - v;
+      const uint64_t tot = __shfl_sync(0xffffffffu, inc, kWarps - 1);
+      const uint64_t base = dev::warp_lookback(a.status, t, tot, a.epoch, a.err);
+      if (lane == 0) {
+        s_base = base;
+        if (t == a.tiles - 1) *a.total_out = base + tot;
+        if (a.write && base + tot > a.capacity) atomicOr(a.err, kErrOverflow);
+      }
+    }
+    __syncthreads();
+    if (a.write) {
+      uint64_t o = s_base + s_wbase[warp];
+      for (uint32_t rr = r0; rr < r1; ++rr) {
+        const uint32_t jl = rr * 32 + lane;
+        const uint32_t hit = jl < nq ? s_hit[jl] : 0;
+        const uint32_t bal = __ballot_sync(0xffffffffu, hit != 0);
+        const uint64_t oo = o + __popc(bal & dev::lanemask_lt());
+        o += __popc(bal);
+        if (!hit || oo >= a.capacity) continue;
+        const uint64_t j = j0 + jl;
+        const uint32_t i = hit - 1;
+        if (a.key_out) static_cast<K*>(a.key_out)[oo] = sk[j];
+        if (a.ids_r) a.ids_r[oo] = i;
+        if (a.ids_s) a.ids_s[oo] = (uint32_t)j;
+        if (VEC) {
+          const uint2 pw = s_pay[jl];
+          if (a.nr_cols == 1 && a.r_bytes[0] == 8) {
+            static_cast<uint64_t*>(a.r_dst[0])[oo] = (uint64_t)pw.x | ((uint64_t)pw.y << 32);
+          } else {
+            if (a.nr_cols > 0) static_cast<uint32_t*>(a.r_dst[0])[oo] = pw.x;
+            if (a.nr_cols > 1) static_cast<uint32_t*>(a.r_dst[1])[oo] = pw.y;
+          }
+        } else {
+          uint64_t h = nslot(sk[j], a.log2cap);  // rare layouts: find the slot again
+          const uint32_t* s;
+          while (true) {
+            s = a.table + h * a.slot_words;
+            if (s[0] == hit) break;
+            h = (h + 1) & mask;
+          }
+          for (int c = 0; c < a.nr_cols; ++c) {
+            const uint32_t* w = s + a.r_word_off[c];
+            if (a.r_bytes[c] == 4)
+              static_cast<uint32_t*>(a.r_dst[c])[oo] = w[0];
+            else
+              static_cast<uint64_t*>(a.r_dst[c])[oo] = (uint64_t)w[0] | ((uint64_t)w[1] << 32);
+          }
+        }
+        for (int c = 0; c < a.ns_cols; ++c) {
+          if (a.s_bytes[c] == 4)
+            static_cast<uint32_t*>(a.s_dst[c])[oo] = static_cast<const uint32_t*>(a.s_src[c])[j];
+          else
+            static_cast<uint64_t*>(a.s_dst[c])[oo] = static_cast<const uint64_t*>(a.s_src[c])[j];
+        }
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -219,6 +353,9 @@ uint64_t run(cj_ctx* ctx, NphjArgs a) {
     a.r_word_off[c] = words;
     words += a.r_bytes[c] / 4;
   }
+  // 4-byte keys with <= 8 payload bytes: pad to 4 words so a slot is one aligned
+  // 16-byte load/store
+  if (sizeof(K) == 4 && words <= 4) words = 4;
   a.slot_words = words;
   const uint64_t cap = 1ull << log2cap;
   Scratch table(ctx, cap * words * 4);
@@ -238,12 +375,21 @@ uint64_t run(cj_ctx* ctx, NphjArgs a) {
     a.status = ctx->status_buffer(a.tiles);
     a.epoch = ctx->next_epoch();
     a.ticket = ctx->ticket(3);
-    int per_sm = 0;
-    CJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_nphj_probe<K>, kThreads, 0));
-    const uint64_t grid = std::min<uint64_t>((uint64_t)ctx->num_sms * std::max(per_sm, 1), a.tiles);
-    ctx->kbegin(a.write ? "nphj_probe" : "nphj_count", 0);
-    k_nphj_probe<K><<<(unsigned)grid, kThreads, 0, ctx->stream>>>(a);
-    ctx->kend();
+    auto launch = [&](auto kern) {
+      int per_sm = 0;
+      CJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0));
+      const uint64_t grid = std::min<uint64_t>((uint64_t)ctx->num_sms * std::max(per_sm, 1), a.tiles);
+      ctx->kbegin(a.write ? "nphj_probe" : "nphj_count", 0);
+      kern<<<(unsigned)grid, kThreads, 0, ctx->stream>>>(a);
+      ctx->kend();
+    };
+    const bool vec = sizeof(K) == 4 && a.slot_words == 4;
+    if (a.unique) {
+      if (vec) launch(k_nphj_probe_u<K, true>);
+      else launch(k_nphj_probe_u<K, false>);
+    } else {
+      launch(k_nphj_probe<K>);
+    }
   }
   CJ_CUDA(cudaGetLastError());
   uint64_t* h = reinterpret_cast<uint64_t*>(ctx->host_pinned);
@@ -255,8 +401,10 @@ uint64_t run(cj_ctx* ctx, NphjArgs a) {
 }  // namespace
 
 uint64_t nphj_find(cj_ctx* ctx, const void* rkeys, uint64_t nr, const void* skeys, uint64_t ns,
-                   int key_bytes, const OutSpec& out, uint64_t capacity, bool count_only) {
+                   int key_bytes, const OutSpec& out, uint64_t capacity, bool count_only,
+                   bool unique) {
   NphjArgs a{};
+  a.unique = unique ? 1 : 0;
   a.rkeys = rkeys;
   a.nr = nr;
   a.skeys = skeys;
