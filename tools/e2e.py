@@ -1,5 +1,5 @@
 import sys, os, json, time
-sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", "/root/repo"))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench, torch
 import paper_2312_00720_b200 as cj
 ctx = cj.Context(0)

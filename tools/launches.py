@@ -1,6 +1,6 @@
 """Summarise an ncu --metrics gpu__time_duration.sum launch list (csv): per
 kernel launches, total ms and share; only launches after the first `skip`
-(tooling, not part of the product).  Usage: python tools_launches.py f.csv [skip]"""
+(tooling, not part of the product).  Usage: python tools/launches.py f.csv [skip]"""
 import csv
 import re
 import sys

@@ -1,5 +1,5 @@
 """Summarise an ncu source page (SASS) by stall samples: top instructions with
-their neighbourhood.  Usage: python tools_ncu_hot.py rep.ncu-rep kernel_regex [n]"""
+their neighbourhood.  Usage: python tools/ncu_hot.py rep.ncu-rep kernel_regex [n]"""
 import csv
 import subprocess
 import sys

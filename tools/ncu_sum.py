@@ -1,5 +1,5 @@
 """Key ncu metrics + stall breakdown per launch of a report (tooling).
-Usage: python tools_ncu_sum.py rep.ncu-rep [launch_index]"""
+Usage: python tools/ncu_sum.py rep.ncu-rep [launch_index]"""
 import csv
 import subprocess
 import sys

@@ -1,5 +1,5 @@
 """Per-SASS-instruction executed counts / stall samples / smem wavefronts of one
-launch in an ncu report (tooling).  Usage: python tools_sass_hot.py rep kernel_regex [min_exec]"""
+launch in an ncu report (tooling).  Usage: python tools/sass_hot.py rep kernel_regex [min_exec]"""
 import csv
 import subprocess
 import sys
