@@ -706,6 +706,24 @@ void launch_v2(cj_ctx* ctx, const BlockPassArgs& a, size_t smem) {
 
 template <class K, int RANK>
 void launch_v2_items(cj_ctx* ctx, const BlockPassArgs& a, size_t smem, int items, int rb) {
+  if (rb == 6) {  // passes of <= 6 bits: 64-digit tables, room for 8192-row tiles
+    switch (items) {
+      case 16: launch_v2<K, 16, RANK, 1, 6>(ctx, a, smem); break;
+      case 12: launch_v2<K, 12, RANK, 1, 6>(ctx, a, smem); break;
+      case 8: launch_v2<K, 8, RANK, 1, 6>(ctx, a, smem); break;
+      default: launch_v2<K, 4, RANK, 1, 6>(ctx, a, smem); break;
+    }
+    return;
+  }
+  if (rb == 7) {  // 7-bit passes (27-bit sort keys: 7+7+7+6)
+    switch (items) {
+      case 16: launch_v2<K, 16, RANK, 1, 7>(ctx, a, smem); break;
+      case 12: launch_v2<K, 12, RANK, 1, 7>(ctx, a, smem); break;
+      case 8: launch_v2<K, 8, RANK, 1, 7>(ctx, a, smem); break;
+      default: launch_v2<K, 4, RANK, 1, 7>(ctx, a, smem); break;
+    }
+    return;
+  }
   if (rb != 8) fail(CJ_ERR_UNSUPPORTED, "scatter pass digits wider than 8 bits");
   switch (items) {
     case 16: launch_v2<K, 16, RANK, 1, 8>(ctx, a, smem); break;
@@ -754,11 +772,11 @@ ScatterGeom scatter_geom(cj_ctx* ctx, uint64_t n, int key_bytes, const ValCols& 
   g.rank = e_rank ? std::atoi(e_rank) : 0;
   g.ctas_per_sm = 1;  // (2 CTAs/SM with single stages measured slower: profiles/)
   g.stages = e_stages ? std::min(2, std::max(1, std::atoi(e_stages))) : 2;
-  const int want_items = e_items ? std::atoi(e_items) : 12;
+  const int want_items = e_items ? std::atoi(e_items) : 16;
   // 227 KB per CTA minus the static arrays (per-warp digit counts 8 KB and
   // ~4 KB of cursors, twice that for 9-bit digits) and the dynamic peer masks
   // of rank mode 0 (16 KB / 32 KB)
-  const size_t budget = (227 - ((size_t)12 << (rb - 8))) * 1024;
+  const size_t budget = (227 - (((size_t)12 << rb) >> 8)) * 1024;
   const size_t match = g.rank == 0 ? (size_t)kTmaWarps * 4 << rb : 0;
   for (int items : {16, 12, 8, 4}) {
     if (items > want_items && items > 4) continue;
@@ -798,11 +816,18 @@ void block_hist(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes, const 
   const uint32_t R = 1u << g.rb;
   CJ_CUDA(cudaMemsetAsync(cnt_dev, 0, sizeof(uint32_t) * R * np * g.nblocks, ctx->stream));
   ctx->kbegin("histogram", n * key_bytes);
-  if (g.rb != 8) fail(CJ_ERR_UNSUPPORTED, "histogram digits wider than 8 bits");
-  if (key_bytes == 4)
-    launch_hist_np<uint32_t, 8>(ctx, static_cast<const uint32_t*>(keys), a, np, cnt_dev);
-  else
-    launch_hist_np<uint64_t, 8>(ctx, static_cast<const uint64_t*>(keys), a, np, cnt_dev);
+  if (g.rb < 6 || g.rb > 8) fail(CJ_ERR_UNSUPPORTED, "histogram digits wider than 8 bits");
+  if (key_bytes == 4) {
+    const uint32_t* k = static_cast<const uint32_t*>(keys);
+    if (g.rb == 6) launch_hist_np<uint32_t, 6>(ctx, k, a, np, cnt_dev);
+    else if (g.rb == 7) launch_hist_np<uint32_t, 7>(ctx, k, a, np, cnt_dev);
+    else launch_hist_np<uint32_t, 8>(ctx, k, a, np, cnt_dev);
+  } else {
+    const uint64_t* k = static_cast<const uint64_t*>(keys);
+    if (g.rb == 6) launch_hist_np<uint64_t, 6>(ctx, k, a, np, cnt_dev);
+    else if (g.rb == 7) launch_hist_np<uint64_t, 7>(ctx, k, a, np, cnt_dev);
+    else launch_hist_np<uint64_t, 8>(ctx, k, a, np, cnt_dev);
+  }
   ctx->kend();
   CJ_CUDA(cudaGetLastError());
 }
@@ -967,12 +992,17 @@ void lsd_partition_group(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t
                          std::vector<uint32_t>* counts_out) {
   if (plan.npasses > 8) fail(CJ_ERR_UNSUPPORTED, "LSD segment longer than 8 passes");
   const int np = plan.npasses;
-  int rb = 8;
-  for (int p = 0; p < np; ++p)
-    if (plan.hi[p] - plan.lo[p] > 8) rb = 9;
+  // digit tables sized to the widest pass: 64 digits for passes of <= 6 bits
+  // (smaller shared-memory tables leave room for longer tiles), else 256
+  int rb = 6;
+  for (int p = 0; p < np; ++p) rb = std::max(rb, (int)(plan.hi[p] - plan.lo[p]));
+  if (plan.npasses > 0 && std::getenv("CJ_RB8")) rb = 8;
+  ScatterGeom g0 = scatter_geom(ctx, n, key_bytes, vals, keys, rb);
+  if (rb != 8 && !g0.tma) {  // the look-back onesweep fallback has 256-digit tables
+    rb = 8;
+    g0 = scatter_geom(ctx, n, key_bytes, vals, keys, rb);
+  }
   const uint32_t kRadix = 1u << rb;
-  const ScatterGeom g0 = scatter_geom(ctx, n, key_bytes, vals, keys, rb);
-  if (rb > 8 && !g0.tma) fail(CJ_ERR_UNSUPPORTED, "9-bit digits need the TMA scatter path");
   std::vector<uint32_t> totals;
   Scratch cnt(ctx, sizeof(uint32_t) * kRadix * std::max(np, 1) * g0.nblocks);
   Scratch tot(ctx, sizeof(uint32_t) * kRadix * std::max(np, 1));
