@@ -159,6 +159,7 @@ struct FindArgs {
   uint16_t* match_e;
   uint8_t* unit_dup;
   uint32_t off_e;            // stage offset of the match_e chunk
+  int blocked;               // CTAs walk contiguous unit ranges (else round robin)
 };
 
 template <class K>
@@ -568,44 +569,66 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constan
   };
   auto is_pre = [&](uint64_t uu) { return WRITE && a.match_e != nullptr && a.unit_dup[uu] == 0; };
 
-  uint64_t u = blockIdx.x;
+  // Unit order: with precomputed unit offsets (two passes) each CTA walks a
+  // contiguous range of units, so the probe chunks of one build chunk (a large
+  // or skewed probe partition) follow each other and reuse the build table;
+  // the single-pass look-back mode needs units in flight in global order
+  // (round robin).
+  const bool blocked = !(WRITE && a.unit_off == nullptr) && a.np_rows > 0 && a.blocked;
+  // blocked ranges split the probe rows evenly (unit q_lo is monotone): units
+  // differ in size (a skewed partition's full chunks vs small ones)
+  auto first_unit = [&](uint64_t c) -> uint64_t {  // first unit with q_lo >= c * |S| / grid
+    const uint64_t target = c * a.np_rows / gridDim.x;
+    uint64_t lo = 0, hi = units;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (descs[mid].q_lo < target) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+  };
+  const uint64_t u_end = blocked ? (blockIdx.x + 1 == gridDim.x ? units : first_unit(blockIdx.x + 1))
+                                 : units;
+  const uint64_t step = blocked ? 1 : gridDim.x;
+  uint64_t u = blocked ? (blockIdx.x == 0 ? 0 : first_unit(blockIdx.x)) : blockIdx.x;
   UnitDesc next{};  // descriptor of the unit after the one in flight (thread 0)
   bool next_pre = false;
   if (tid == 0) {
     dev::mbar_init(&mbar[0], 1);
     dev::mbar_init(&mbar[1], 1);
     dev::fence_mbar_init();
-    if (u < units) {
+    if (u < u_end) {
       s_desc[0] = descs[u];
       s_pre[0] = is_pre(u);
       issue(0, s_desc[0], s_pre[0]);
     }
-    if (u + gridDim.x < units) {
-      next = descs[u + gridDim.x];
-      next_pre = is_pre(u + gridDim.x);
+    if (u + step < u_end) {
+      next = descs[u + step];
+      next_pre = is_pre(u + step);
     }
   }
   __syncthreads();
   uint32_t phase[2] = {0, 0};
   int b = 0;
-  auto issue_next = [&](int nb_) {  // thread 0: copies of unit u + gridDim.x into stage nb_
-    if (u + gridDim.x < units) {
+  auto issue_next = [&](int nb_) {  // thread 0: copies of unit u + step into stage nb_
+    if (u + step < u_end) {
       s_desc[nb_] = next;
       s_pre[nb_] = next_pre;
       dev::fence_proxy_async();
       issue(nb_, next, next_pre);
-      if (u + 2ull * gridDim.x < units) {  // in flight
-        next = descs[u + 2ull * gridDim.x];
-        next_pre = is_pre(u + 2ull * gridDim.x);
+      if (u + 2 * step < u_end) {  // in flight
+        next = descs[u + 2 * step];
+        next_pre = is_pre(u + 2 * step);
       }
     }
   };
-  for (; u < units; u += gridDim.x, b = (b + 1) % a.stages) {
+  uint64_t built_lo = ~0ull, built_hi = 0;  // build chunk whose table is in shared memory
+  for (; u < u_end; u += step, b = (b + 1) % a.stages) {
     const UnitDesc inf = s_desc[b];
     const bool pre = s_pre[b];
+    const bool reuse = inf.b_lo == built_lo && inf.b_hi == built_hi;
     if (tid == 0) {
       if (a.stages == 2) issue_next(b ^ 1);
-      s_dup = 0;
+      if (!reuse) s_dup = 0;
     }
     uint64_t unit_base = 0;
     if (WRITE && tid == 32 && a.unit_off) unit_base = a.unit_off[u];
@@ -646,15 +669,18 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constan
     uint32_t cap_log2 = 1;
     while ((1u << cap_log2) < 2 * nb) ++cap_log2;
     const uint32_t cap = 1u << cap_log2, cmask = cap - 1;
-    for (uint32_t i = tid; i < cap; i += kTmaThreads) tab[i] = kNoMatch;
+    if (!reuse)
+      for (uint32_t i = tid; i < cap; i += kTmaThreads) tab[i] = kNoMatch;
     dev::mbar_wait(&mbar[b], phase[b]);
     phase[b] ^= 1;
     __syncthreads();
 
     // 1. insert chunk positions (CAS); meeting an equal key marks duplicates
-    //    (a plain-store first round measured slower: profiles/r01b_summary.md)
+    //    (a plain-store first round measured slower: profiles/r01b_summary.md).
+    //    The previous unit of this CTA left the same build chunk's table (or
+    //    its sorted positions) in shared memory: reuse it.
     bool dup = false;
-    for (uint32_t i = tid; i < nb; i += kTmaThreads) {
+    for (uint32_t i = reuse ? nb : tid; i < nb; i += kTmaThreads) {
       const K k = bk[i];
       uint32_t sl = slot_of(k, cap_log2);
       while (true) {
@@ -669,7 +695,9 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constan
     const bool has_dup = s_dup != 0;
     if (!WRITE && a.unit_dup && tid == 0) a.unit_dup[u] = has_dup ? 1 : 0;
     uint16_t* sidx = reinterpret_cast<uint16_t*>(tab);
-    if (has_dup) {  // stably sorted chunk positions: bitonic over (key, position)
+    built_lo = inf.b_lo;
+    built_hi = inf.b_hi;
+    if (has_dup && !reuse) {  // stably sorted chunk positions: bitonic over (key, position)
       uint32_t np2 = 1;
       while (np2 < nb) np2 <<= 1;
       for (uint32_t i = tid; i < np2; i += kTmaThreads) sidx[i] = i < nb ? (uint16_t)i : kEmpty16;
@@ -1035,6 +1063,8 @@ FindArgs base_args(const void* bkeys, const uint64_t* boff, const void* pkeys,
   a.limit = limit;
   a.qchunk = probe_chunk();
   a.stages = find_stages();
+  const char* order = std::getenv("CJ_FIND_ORDER");
+  a.blocked = order && std::strcmp(order, "blocked") == 0;
   return a;
 }
 
