@@ -437,10 +437,77 @@ __global__ void k_phj_desc(const uint64_t* __restrict__ boff, const uint64_t* __
   }
 }
 
+// Rows [0, cnt) of a unit's output at ubase, column by column, consecutive
+// threads on consecutive output rows: row t is (build idx, probe idx) =
+// (me[t], t) when ident, else list[t] = build idx << 16 | probe idx.
+template <class K>
+__device__ __forceinline__ void emit_rows(const FindArgs& a, const UnitDesc& inf,
+                                          const uint8_t* st, const K* pk, const uint16_t* me,
+                                          const uint32_t* list, uint64_t ubase, uint32_t cnt,
+                                          bool ident) {
+  const int tid = threadIdx.x;
+  const uint32_t bsh4 = (uint32_t)(inf.b_lo & 3), bsh8 = (uint32_t)(inf.b_lo & 1);
+  const uint32_t qsh4 = (uint32_t)(inf.q_lo & 3), qsh8 = (uint32_t)(inf.q_lo & 1);
+  // 3b. column by column, consecutive threads write consecutive output rows
+  if (ubase + cnt > a.capacity) cnt = ubase < a.capacity ? (uint32_t)(a.capacity - ubase) : 0u;
+  constexpr int kE = 8;
+  for (uint32_t t0 = 0; t0 < cnt; t0 += kE * kTmaThreads) {
+    uint32_t L[kE];
+#pragma unroll
+    for (int k = 0; k < kE; ++k) {
+      const uint32_t t = t0 + tid + k * kTmaThreads;
+      L[k] = t < cnt ? (ident ? ((uint32_t)me[t] << 16) | t : list[t]) : 0u;
+    }
+    auto each = [&](auto&& f) {
+#pragma unroll
+      for (int k = 0; k < kE; ++k) {
+        const uint32_t t = t0 + tid + k * kTmaThreads;
+        if (t < cnt) f(ubase + t, L[k] >> 16, L[k] & 0xffffu);
+      }
+    };
+    if (a.key_out) {
+      K* ko = static_cast<K*>(a.key_out);
+      each([&](uint64_t oo, uint32_t, uint32_t jl) { ko[oo] = pk[jl]; });
+    }
+    if (a.ids_r)
+      each([&](uint64_t oo, uint32_t li, uint32_t) {
+        const uint64_t gi = inf.b_lo + li;
+        a.ids_r[oo] = a.carried_r ? a.carried_r[gi] : (uint32_t)gi;
+      });
+    if (a.ids_s)
+      each([&](uint64_t oo, uint32_t, uint32_t jl) {
+        const uint64_t j = inf.q_lo + jl;
+        a.ids_s[oo] = a.carried_s ? a.carried_s[j] : (uint32_t)j;
+      });
+    for (int c = 0; c < a.nr; ++c) {
+      if (a.r_bytes[c] == 4) {
+        const uint32_t* sv = reinterpret_cast<const uint32_t*>(st + a.off_r[c]) + bsh4;
+        uint32_t* dv = static_cast<uint32_t*>(a.r_dst[c]);
+        each([&](uint64_t oo, uint32_t li, uint32_t) { dv[oo] = sv[li]; });
+      } else {
+        const uint64_t* sv = reinterpret_cast<const uint64_t*>(st + a.off_r[c]) + bsh8;
+        uint64_t* dv = static_cast<uint64_t*>(a.r_dst[c]);
+        each([&](uint64_t oo, uint32_t li, uint32_t) { dv[oo] = sv[li]; });
+      }
+    }
+    for (int c = 0; c < a.ns; ++c) {
+      if (a.s_bytes[c] == 4) {
+        const uint32_t* sv = reinterpret_cast<const uint32_t*>(st + a.off_s[c]) + qsh4;
+        uint32_t* dv = static_cast<uint32_t*>(a.s_dst[c]);
+        each([&](uint64_t oo, uint32_t, uint32_t jl) { dv[oo] = sv[jl]; });
+      } else {
+        const uint64_t* sv = reinterpret_cast<const uint64_t*>(st + a.off_s[c]) + qsh8;
+        uint64_t* dv = static_cast<uint64_t*>(a.s_dst[c]);
+        each([&](uint64_t oo, uint32_t, uint32_t jl) { dv[oo] = sv[jl]; });
+      }
+    }
+  }
+}
+
 // GFTR/GFUR emission of a unit without duplicate build keys: compact the hits
-// in probe order (list[t] = build idx << 16 | probe idx), then write column by
-// column, consecutive threads on consecutive output rows.  The match of probe
-// row jl is me[jl] (0xffff: none) when the count pass resolved it, else res[jl].
+// in probe order (list[t] = build idx << 16 | probe idx), then emit_rows.  The
+// match of probe row jl is me[jl] (0xffff: none) when the count pass resolved
+// it, else res[jl].
 template <class K>
 __device__ __forceinline__ void emit_compact(const FindArgs& a, const UnitDesc& inf,
                                              const uint8_t* st, const K* pk, const uint16_t* me,
@@ -448,81 +515,26 @@ __device__ __forceinline__ void emit_compact(const FindArgs& a, const UnitDesc& 
                                              uint32_t nq, const uint64_t* s_wbase,
                                              const uint64_t* s_wcount, uint32_t* list) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t bsh4 = (uint32_t)(inf.b_lo & 3), bsh8 = (uint32_t)(inf.b_lo & 1);
-  const uint32_t qsh4 = (uint32_t)(inf.q_lo & 3), qsh8 = (uint32_t)(inf.q_lo & 1);
-    const uint64_t ubase = s_wbase[0];
-    uint32_t cnt = (uint32_t)(s_wbase[kTmaWarps - 1] - ubase + s_wcount[kTmaWarps - 1]);
-    // every probe row matched once (PK-FK, match ratio 1): output row t is probe
-    // row t, its build row is me[t]; no compaction needed
-    const bool ident = me != nullptr && cnt == nq;
-    if (!ident) {
-      // 3a. compact the hits in probe order: list[t] = (build idx << 16) | probe idx
-      uint32_t o = (uint32_t)(s_wbase[warp] - ubase);
-      for (uint32_t r = r0; r < r1; ++r) {
-        const uint32_t jl = r * 32 + lane;
-        uint32_t e = kNoMatch;
-        if (jl < nq) e = me ? (me[jl] == kEmpty16 ? kNoMatch : (uint32_t)me[jl]) : res[jl];
-        const bool hit = e != kNoMatch;
-        const uint32_t bal = __ballot_sync(0xffffffffu, hit);
-        if (hit) list[o + __popc(bal & dev::lanemask_lt())] = (e << 16) | jl;
-        o += __popc(bal);
-      }
-      __syncthreads();
+  const uint64_t ubase = s_wbase[0];
+  uint32_t cnt = (uint32_t)(s_wbase[kTmaWarps - 1] - ubase + s_wcount[kTmaWarps - 1]);
+  // every probe row matched once (PK-FK, match ratio 1): output row t is probe
+  // row t, its build row is me[t]; no compaction needed
+  const bool ident = me != nullptr && cnt == nq;
+  if (!ident) {
+    // 3a. compact the hits in probe order: list[t] = (build idx << 16) | probe idx
+    uint32_t o = (uint32_t)(s_wbase[warp] - ubase);
+    for (uint32_t r = r0; r < r1; ++r) {
+      const uint32_t jl = r * 32 + lane;
+      uint32_t e = kNoMatch;
+      if (jl < nq) e = me ? (me[jl] == kEmpty16 ? kNoMatch : (uint32_t)me[jl]) : res[jl];
+      const bool hit = e != kNoMatch;
+      const uint32_t bal = __ballot_sync(0xffffffffu, hit);
+      if (hit) list[o + __popc(bal & dev::lanemask_lt())] = (e << 16) | jl;
+      o += __popc(bal);
     }
-    // 3b. column by column, consecutive threads write consecutive output rows
-    if (ubase + cnt > a.capacity) cnt = ubase < a.capacity ? (uint32_t)(a.capacity - ubase) : 0u;
-    constexpr int kE = 8;
-    for (uint32_t t0 = 0; t0 < cnt; t0 += kE * kTmaThreads) {
-      uint32_t L[kE];
-#pragma unroll
-      for (int k = 0; k < kE; ++k) {
-        const uint32_t t = t0 + tid + k * kTmaThreads;
-        L[k] = t < cnt ? (ident ? ((uint32_t)me[t] << 16) | t : list[t]) : 0u;
-      }
-      auto each = [&](auto&& f) {
-#pragma unroll
-        for (int k = 0; k < kE; ++k) {
-          const uint32_t t = t0 + tid + k * kTmaThreads;
-          if (t < cnt) f(ubase + t, L[k] >> 16, L[k] & 0xffffu);
-        }
-      };
-      if (a.key_out) {
-        K* ko = static_cast<K*>(a.key_out);
-        each([&](uint64_t oo, uint32_t, uint32_t jl) { ko[oo] = pk[jl]; });
-      }
-      if (a.ids_r)
-        each([&](uint64_t oo, uint32_t li, uint32_t) {
-          const uint64_t gi = inf.b_lo + li;
-          a.ids_r[oo] = a.carried_r ? a.carried_r[gi] : (uint32_t)gi;
-        });
-      if (a.ids_s)
-        each([&](uint64_t oo, uint32_t, uint32_t jl) {
-          const uint64_t j = inf.q_lo + jl;
-          a.ids_s[oo] = a.carried_s ? a.carried_s[j] : (uint32_t)j;
-        });
-      for (int c = 0; c < a.nr; ++c) {
-        if (a.r_bytes[c] == 4) {
-          const uint32_t* sv = reinterpret_cast<const uint32_t*>(st + a.off_r[c]) + bsh4;
-          uint32_t* dv = static_cast<uint32_t*>(a.r_dst[c]);
-          each([&](uint64_t oo, uint32_t li, uint32_t) { dv[oo] = sv[li]; });
-        } else {
-          const uint64_t* sv = reinterpret_cast<const uint64_t*>(st + a.off_r[c]) + bsh8;
-          uint64_t* dv = static_cast<uint64_t*>(a.r_dst[c]);
-          each([&](uint64_t oo, uint32_t li, uint32_t) { dv[oo] = sv[li]; });
-        }
-      }
-      for (int c = 0; c < a.ns; ++c) {
-        if (a.s_bytes[c] == 4) {
-          const uint32_t* sv = reinterpret_cast<const uint32_t*>(st + a.off_s[c]) + qsh4;
-          uint32_t* dv = static_cast<uint32_t*>(a.s_dst[c]);
-          each([&](uint64_t oo, uint32_t, uint32_t jl) { dv[oo] = sv[jl]; });
-        } else {
-          const uint64_t* sv = reinterpret_cast<const uint64_t*>(st + a.off_s[c]) + qsh8;
-          uint64_t* dv = static_cast<uint64_t*>(a.s_dst[c]);
-          each([&](uint64_t oo, uint32_t, uint32_t jl) { dv[oo] = sv[jl]; });
-        }
-      }
-    }
+    __syncthreads();
+  }
+  emit_rows<K>(a, inf, st, pk, me, list, ubase, cnt, ident);
 }
 
 template <class K, bool WRITE>
@@ -644,8 +656,18 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constan
       // continue at the compaction below (res <- match_e)
       const uint16_t* me = reinterpret_cast<const uint16_t*>(st + a.off_e) +
                            (inf.q_lo - dev::align_lo(inf.q_lo, 2));
+      // the count pass's per-unit total: every probe row matched once -> the
+      // output rows are the probe rows in order, no count / scan / compaction
+      const uint64_t ucnt = a.unit_counts ? a.unit_counts[u] : ~0ull;
+      const uint64_t ubase = a.unit_counts ? a.unit_off[u] : 0;
       dev::mbar_wait(&mbar[b], phase[b]);
       phase[b] ^= 1;
+      if (ucnt == nq) {
+        emit_rows<K>(a, inf, st, pk, me, nullptr, ubase, nq, true);
+        __syncthreads();
+        if (a.stages == 1 && tid == 0) issue_next(0);
+        continue;
+      }
       uint64_t wc = 0;
       for (uint32_t r = r0; r < r1; ++r) {
         const uint32_t jl = r * 32 + lane;
@@ -988,6 +1010,8 @@ uint64_t run_find(cj_ctx* ctx, FindArgs a, uint64_t total_units) {
         // bounded by the capacity on the device, and an overflow is reported
         // (CapacityExceeded) after the single synchronisation below
         a.unit_off = offs.as<uint64_t>();
+        a.unit_counts = std::getenv("CJ_FIND_FAST") && std::strcmp(std::getenv("CJ_FIND_FAST"), "0") == 0
+                            ? nullptr : counts.as<uint64_t>();
         CJ_CUDA(cudaFuncSetAttribute(k_phj_tma<K, true>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tma_smem));
         ctx->kbegin("phj_find", 0);

@@ -279,6 +279,68 @@ __device__ __forceinline__ uint32_t gallop(const K* __restrict__ r, uint32_t fro
 constexpr uint32_t kSmjPer = kTileS / kTmaThreads;  // probes per thread (4)
 constexpr uint32_t kSmjList = 2 * kTileS;            // compacted rows per tile in shared memory
 
+// Rows [0, cnt) of a tile's output at tbase, column by column, consecutive
+// threads on consecutive output rows; row_of(t) = r window idx << 16 | probe idx.
+template <class K, class RowOf>
+__device__ __forceinline__ void smj_emit_rows(const SmjArgs& a, const SmjDesc& d, const uint8_t* st,
+                                              const K* sk, uint64_t tbase, uint32_t cnt,
+                                              RowOf row_of) {
+  const int tid = threadIdx.x;
+  const uint32_t ssh4 = (uint32_t)(d.s_lo & 3), ssh8 = (uint32_t)(d.s_lo & 1);
+  const uint32_t rsh4 = (uint32_t)(d.r_lo & 3), rsh8 = (uint32_t)(d.r_lo & 1);
+  if (tbase + cnt > a.capacity) cnt = tbase < a.capacity ? (uint32_t)(a.capacity - tbase) : 0u;
+  constexpr int kE = kSmjList / kTmaThreads;
+  uint32_t L[kE];
+#pragma unroll
+  for (int k = 0; k < kE; ++k) {
+    const uint32_t tt = tid + k * kTmaThreads;
+    L[k] = tt < cnt ? row_of(tt) : 0u;
+  }
+  auto each = [&](auto&& f) {
+#pragma unroll
+    for (int k = 0; k < kE; ++k) {
+      const uint32_t tt = tid + k * kTmaThreads;
+      if (tt < cnt) f(tbase + tt, L[k] >> 16, L[k] & 0xffffu);
+    }
+  };
+  if (a.key_out) {
+    K* ko = static_cast<K*>(a.key_out);
+    each([&](uint64_t oo, uint32_t, uint32_t jl) { ko[oo] = sk[jl]; });
+  }
+  if (a.ids_r)
+    each([&](uint64_t oo, uint32_t li, uint32_t) {
+      const uint64_t i = d.r_lo + li;
+      a.ids_r[oo] = a.carried_r ? a.carried_r[i] : (uint32_t)i;
+    });
+  if (a.ids_s)
+    each([&](uint64_t oo, uint32_t, uint32_t jl) {
+      const uint64_t j = d.s_lo + jl;
+      a.ids_s[oo] = a.carried_s ? a.carried_s[j] : (uint32_t)j;
+    });
+  for (int c = 0; c < a.nr_cols; ++c) {
+    if (a.r_bytes[c] == 4) {
+      const uint32_t* sv = reinterpret_cast<const uint32_t*>(st + a.off_r[c]) + rsh4;
+      uint32_t* dv = static_cast<uint32_t*>(a.r_dst[c]);
+      each([&](uint64_t oo, uint32_t li, uint32_t) { dv[oo] = sv[li]; });
+    } else {
+      const uint64_t* sv = reinterpret_cast<const uint64_t*>(st + a.off_r[c]) + rsh8;
+      uint64_t* dv = static_cast<uint64_t*>(a.r_dst[c]);
+      each([&](uint64_t oo, uint32_t li, uint32_t) { dv[oo] = sv[li]; });
+    }
+  }
+  for (int c = 0; c < a.ns_cols; ++c) {
+    if (a.s_bytes[c] == 4) {
+      const uint32_t* sv = reinterpret_cast<const uint32_t*>(st + a.off_s[c]) + ssh4;
+      uint32_t* dv = static_cast<uint32_t*>(a.s_dst[c]);
+      each([&](uint64_t oo, uint32_t, uint32_t jl) { dv[oo] = sv[jl]; });
+    } else {
+      const uint64_t* sv = reinterpret_cast<const uint64_t*>(st + a.off_s[c]) + ssh8;
+      uint64_t* dv = static_cast<uint64_t*>(a.s_dst[c]);
+      each([&](uint64_t oo, uint32_t, uint32_t jl) { dv[oo] = sv[jl]; });
+    }
+  }
+}
+
 template <class K, bool WRITE>
 __global__ void __launch_bounds__(kTmaThreads, 1) k_smj_tma(const __grid_constant__ SmjArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -364,8 +426,22 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_smj_tma(const __grid_constan
     const bool win = w <= a.wmax;
     const K* sk = reinterpret_cast<const K*>(st + a.off_sk) + (d.s_lo - dev::align_lo(d.s_lo, kb));
     const K* rk = reinterpret_cast<const K*>(st + a.off_rk) + (d.r_lo - dev::align_lo(d.r_lo, kb));
+    // the count pass's tile total: every probe matched once (PK-FK tile whose
+    // r window is staged; the count pass may take wider windows) -> the
+    // output rows are the probe rows in order, their r rows are match_e; no
+    // bounds, scan or compaction
+    const bool fast_ok = WRITE && pre && win && a.tile_counts != nullptr;
+    const uint64_t fcnt = fast_ok ? a.tile_counts[t] : ~0ull;
+    const uint64_t fbase = fast_ok ? a.tile_off[t] : 0;
     dev::mbar_wait(&mbar[b], phase[b]);
     phase[b] ^= 1;
+    if (WRITE && fcnt == nq) {
+      const uint16_t* me = reinterpret_cast<const uint16_t*>(st + a.off_e) +
+                           (d.s_lo - dev::align_lo(d.s_lo, 2));
+      smj_emit_rows<K>(a, d, st, sk, fbase, nq, [&](uint32_t tt) { return ((uint32_t)me[tt] << 16) | tt; });
+      __syncthreads();
+      continue;
+    }
     __syncthreads();
 
     // 1. bounds of this thread's four probes
@@ -456,58 +532,13 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_smj_tma(const __grid_constan
         __syncthreads();
       }
       // 2b. column by column, consecutive threads on consecutive output rows
-      uint32_t cnt = (uint32_t)tcount;
-      if (tbase + cnt > a.capacity) cnt = tbase < a.capacity ? (uint32_t)(a.capacity - tbase) : 0u;
-      constexpr int kE = kSmjList / kTmaThreads;
-      uint32_t L[kE];
-#pragma unroll
-      for (int k = 0; k < kE; ++k) {
-        const uint32_t tt = tid + k * kTmaThreads;
-        L[k] = tt < cnt ? (ident ? (loff[tt] << 16) | tt : list[tt]) : 0u;
-      }
-      auto each = [&](auto&& f) {
-#pragma unroll
-        for (int k = 0; k < kE; ++k) {
-          const uint32_t tt = tid + k * kTmaThreads;
-          if (tt < cnt) f(tbase + tt, L[k] >> 16, L[k] & 0xffffu);
-        }
-      };
-      if (a.key_out) {
-        K* ko = static_cast<K*>(a.key_out);
-        each([&](uint64_t oo, uint32_t, uint32_t jl) { ko[oo] = sk[jl]; });
-      }
-      if (a.ids_r)
-        each([&](uint64_t oo, uint32_t li, uint32_t) {
-          const uint64_t i = d.r_lo + li;
-          a.ids_r[oo] = a.carried_r ? a.carried_r[i] : (uint32_t)i;
-        });
-      if (a.ids_s)
-        each([&](uint64_t oo, uint32_t, uint32_t jl) {
-          const uint64_t j = d.s_lo + jl;
-          a.ids_s[oo] = a.carried_s ? a.carried_s[j] : (uint32_t)j;
-        });
-      for (int c = 0; c < a.nr_cols; ++c) {
-        if (a.r_bytes[c] == 4) {
-          const uint32_t* sv = reinterpret_cast<const uint32_t*>(st + a.off_r[c]) + rsh4;
-          uint32_t* dv = static_cast<uint32_t*>(a.r_dst[c]);
-          each([&](uint64_t oo, uint32_t li, uint32_t) { dv[oo] = sv[li]; });
-        } else {
-          const uint64_t* sv = reinterpret_cast<const uint64_t*>(st + a.off_r[c]) + rsh8;
-          uint64_t* dv = static_cast<uint64_t*>(a.r_dst[c]);
-          each([&](uint64_t oo, uint32_t li, uint32_t) { dv[oo] = sv[li]; });
-        }
-      }
-      for (int c = 0; c < a.ns_cols; ++c) {
-        if (a.s_bytes[c] == 4) {
-          const uint32_t* sv = reinterpret_cast<const uint32_t*>(st + a.off_s[c]) + ssh4;
-          uint32_t* dv = static_cast<uint32_t*>(a.s_dst[c]);
-          each([&](uint64_t oo, uint32_t, uint32_t jl) { dv[oo] = sv[jl]; });
-        } else {
-          const uint64_t* sv = reinterpret_cast<const uint64_t*>(st + a.off_s[c]) + ssh8;
-          uint64_t* dv = static_cast<uint64_t*>(a.s_dst[c]);
-          each([&](uint64_t oo, uint32_t, uint32_t jl) { dv[oo] = sv[jl]; });
-        }
-      }
+      const uint32_t* lst = list;
+      const uint32_t* lof = loff;
+      if (ident)
+        smj_emit_rows<K>(a, d, st, sk, tbase, (uint32_t)tcount,
+                         [&](uint32_t tt) { return (lof[tt] << 16) | tt; });
+      else
+        smj_emit_rows<K>(a, d, st, sk, tbase, (uint32_t)tcount, [&](uint32_t tt) { return lst[tt]; });
       __syncthreads();
       continue;
     }
@@ -639,6 +670,8 @@ uint64_t run_tma(cj_ctx* ctx, SmjArgs a) {
     // launched without waiting for the total: writes are bounded by the
     // capacity on the device; an overflow is reported after the one sync below
     a.tile_off = offs.as<uint64_t>();
+    const char* ff = std::getenv("CJ_FIND_FAST");
+    a.tile_counts = handoff && !(ff && std::strcmp(ff, "0") == 0) ? counts.as<uint64_t>() : nullptr;
     const size_t smem = smj_layout<K>(a, true);
     if (smem > 220 * 1024) fail(CJ_ERR_UNSUPPORTED, "merge join stage exceeds shared memory");
     CJ_CUDA(cudaFuncSetAttribute(k_smj_tma<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
