@@ -104,6 +104,8 @@ def parse():
     p.add_argument("--scale-log2", type=int, default=0,
                    help="shrink |R|,|S| by 2^k (debug only; the headline uses 0)")
     p.add_argument("--no-extras", action="store_true", help="skip variants/e2e/cpu legs")
+    p.add_argument("--e2e-steps", type=int, default=16,
+                   help="end-to-end steps (two lanes; more steps amortise the lanes' ramp)")
     return p.parse_args()
 
 
@@ -464,7 +466,7 @@ def main():
                                      if va != "nphj" else None)}
         out["variants"] = var
         # end to end through the host-buffer C-ABI (pinned host in/out)
-        out["e2e"] = e2e_leg(ctx, R, S, opt)
+        out["e2e"] = e2e_leg(ctx, R, S, opt, steps=a.e2e_steps)
         out["cpu_baseline"] = cpu_baseline(nr, ns, a.variant)
     if rank == 0:
         print(json.dumps(out))
