@@ -198,6 +198,9 @@ typedef struct {
   uint64_t transform_ns, find_ns, materialize_ns;   /* PhaseReport (mem_ledger.hpp:231-246) */
   double clusteredness_r, clusteredness_s;          /* JoinStats (join_engine.hpp:54-58) */
   uint64_t device_bytes_peak;      /* scratch + outputs held by the call */
+  /* PhaseReport::peak_by_phase (mem_ledger.hpp:231-246): device bytes the call
+   * held at its high-water mark in each phase */
+  uint64_t peak_transform_b, peak_find_b, peak_materialize_b;
 } cj_join_result;
 
 void cj_default_options(cj_join_options* opt);

@@ -10,6 +10,11 @@
 //   refjoin star  --fact N --dims D --dim-rows M --seed S --algo phj|smj --pattern gftr|gfur
 //                 [--reps N] [--threads T]   (workloads::gen_star + the reference's
 //                 run_join_sequence loop, sequence.cpp:9-67, keeping the last output)
+//   refjoin export [workload opts] --dir DIR   (workloads::export_relation of R, S
+//                 into DIR/R, DIR/S; prints the generator digests)
+//   refjoin import --dir DIR                  (workloads::import_relation; prints
+//                 name, rows, key_unique, column kinds and digests)
+//   refjoin report --in CSV                   (benchio::read_csv + render_report)
 //   (--swap builds on S, whose keys repeat, and probes with R)
 //
 // Workload options mirror workloads::WorkloadSpec (workloads.hpp:11-21):
@@ -31,12 +36,17 @@
 #include <string>
 #include <vector>
 
+#include <iostream>
+#include <sstream>
+
+#include "coljoin/bench_io.hpp"
 #include "coljoin/hash_match.hpp"
 #include "coljoin/join_engine.hpp"
 #include "coljoin/merge_match.hpp"
 #include "coljoin/oracle.hpp"
 #include "coljoin/primitives.hpp"
 #include "coljoin/reference.hpp"
+#include "coljoin/relation_io.hpp"
 #include "coljoin/rng.hpp"
 #include "coljoin/sequence.hpp"
 #include "coljoin/workloads.hpp"
@@ -385,6 +395,39 @@ int cmd_prim(const Args& a) {
   return 0;
 }
 
+// Relation manifests and the bench CSV through the reference's own
+// relation_io.cpp / bench_io.cpp: the interop checks of tests/test_formats.py.
+int cmd_export(const Args& a) {
+  auto [r, s] = make_workload(a);
+  const std::string dir = a.get("--dir", "");
+  if (dir.empty()) throw SpecInvalid("--dir is required");
+  workloads::export_relation(r, std::filesystem::path(dir) / "R");
+  workloads::export_relation(s, std::filesystem::path(dir) / "S");
+  return cmd_gen(a);
+}
+
+int cmd_import(const Args& a) {
+  const Relation r = workloads::import_relation(a.get("--dir", ""));
+  std::printf("{\"name\": \"%s\", \"rows\": %zu, \"key_unique\": %d, \"columns\": [",
+              r.name.c_str(), r.rows(), r.key_unique ? 1 : 0);
+  auto col = [](const Column& c, bool first) {
+    std::printf("%s{\"kind\": \"%s\", \"digest\": \"%016llx\"}", first ? "" : ", ",
+                c.kind() == ValueKind::u64 ? "u64" : "u32",
+                (unsigned long long)digest_col(c));
+  };
+  col(r.key, true);
+  for (const auto& p : r.payloads) col(p, false);
+  std::printf("]}\n");
+  return 0;
+}
+
+int cmd_report(const Args& a) {
+  std::ifstream in(a.get("--in", ""));
+  if (!in) throw SchemaError("cannot open the CSV");
+  std::cout << benchio::render_report(benchio::read_csv(in));
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -399,6 +442,9 @@ int main(int argc, char** argv) {
     if (std::strcmp(argv[1], "gen") == 0) return cmd_gen(a);
     if (std::strcmp(argv[1], "prim") == 0) return cmd_prim(a);
     if (std::strcmp(argv[1], "star") == 0) return cmd_star(a);
+    if (std::strcmp(argv[1], "export") == 0) return cmd_export(a);
+    if (std::strcmp(argv[1], "import") == 0) return cmd_import(a);
+    if (std::strcmp(argv[1], "report") == 0) return cmd_report(a);
   } catch (const std::exception& e) {
     std::fprintf(stderr, "refjoin: %s\n", e.what());
     return 1;

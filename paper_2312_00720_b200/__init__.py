@@ -7,12 +7,12 @@ reference operator API; see DESIGN.md.
 from ._capi import (CJ_MAX_COLS, Error, LengthMismatch, KindError, FanoutTooLarge,  # noqa: F401
                     IndexOutOfBounds, EmptyInput, NotSorted, DuplicateBuildKeys,
                     FanoutMismatch, CapacityExceeded, TransformMismatch, SpecInvalid,
-                    Unsupported, build, lib, exported_symbols)
+                    Unsupported, UnknownShape, SchemaError, build, lib, exported_symbols)
 from .coljoin import (Context, Relation, JoinOutput, PhaseReport, histogram,  # noqa: F401
                       exclusive_prefix_sum, radix_partition, radix_partition_passes, sort_pairs,
                       sort_keys, gather, gather_clusteredness, partition_relation,
                       hash_find_matches, merge_find_matches, run_join, run_join_host,
                       gen_pk_fk, to_device, to_host, options, run_join_sequence, gen_star,
-                      SequenceStep)
+                      SequenceStep, export_relation, import_relation)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -72,7 +72,8 @@ class JoinResult(C.Structure):
                 ("ids_r", C.c_void_p), ("ids_s", C.c_void_p), ("transform_ns", C.c_uint64),
                 ("find_ns", C.c_uint64), ("materialize_ns", C.c_uint64),
                 ("clusteredness_r", C.c_double), ("clusteredness_s", C.c_double),
-                ("device_bytes_peak", C.c_uint64)]
+                ("device_bytes_peak", C.c_uint64), ("peak_transform_b", C.c_uint64),
+                ("peak_find_b", C.c_uint64), ("peak_materialize_b", C.c_uint64)]
 
 
 class SequenceStep(C.Structure):

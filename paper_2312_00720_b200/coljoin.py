@@ -292,9 +292,12 @@ class Relation:
 
 @dataclass
 class PhaseReport:
+    """mem_ledger.hpp:231-246: phase times and, per phase, the device bytes the
+    call held at its high-water mark (peak_by_phase)."""
     transform_ns: int = 0
     find_ns: int = 0
     materialize_ns: int = 0
+    peak_by_phase: tuple = (0, 0, 0)
 
     def total_ns(self) -> int:
         return self.transform_ns + self.find_ns + self.materialize_ns
@@ -368,7 +371,9 @@ def run_join(ctx: Context, build: Relation, probe: Relation, algo="phj", pattern
     ids_r = _wrap(ctx, res.ids_r, t, 4) if res.ids_r else None
     ids_s = _wrap(ctx, res.ids_s, t, 4) if res.ids_s else None
     rel = Relation(key, pays, name=(build.name + "_" + probe.name) or "join")
-    return JoinOutput(rel, PhaseReport(res.transform_ns, res.find_ns, res.materialize_ns), t,
+    return JoinOutput(rel, PhaseReport(res.transform_ns, res.find_ns, res.materialize_ns,
+                                       (res.peak_transform_b, res.peak_find_b,
+                                        res.peak_materialize_b)), t,
                       res.clusteredness_r if kw.get("want_stats") else 1.0,
                       res.clusteredness_s if kw.get("want_stats") else 1.0, ids_r, ids_s)
 
@@ -410,8 +415,10 @@ def run_join_host(ctx: Context, build: Relation, probe: Relation, algo="phj", pa
     pays += [arena.take(res.pay[R.npay + i], t, S.pay_bytes[i]) for i in range(S.npay)]
     ids_r = arena.take(res.ids_r, t, 4) if res.ids_r else None
     ids_s = arena.take(res.ids_s, t, 4) if res.ids_s else None
-    out = JoinOutput(Relation(key, pays), PhaseReport(res.transform_ns, res.find_ns,
-                                                      res.materialize_ns), t,
+    out = JoinOutput(Relation(key, pays),
+                     PhaseReport(res.transform_ns, res.find_ns, res.materialize_ns,
+                                 (res.peak_transform_b, res.peak_find_b, res.peak_materialize_b)),
+                     t,
                      res.clusteredness_r, res.clusteredness_s, ids_r, ids_s)
     return out, h2d.value, d2h.value
 
@@ -479,3 +486,73 @@ def gen_star(ctx: Context, fact_rows: int, dims: int, dim_rows: int, seed: int =
                               ids.data_ptr(), _ptrs(fks), _ptrs(dk), _ptrs(dp)), ctx.h, "gen_star")
     fact = Relation(ids, fks, "fact", True)
     return fact, [Relation(dk[d], [dp[d]], f"dim{d + 1}", True) for d in range(dims)]
+
+
+# ---- relation manifests (relation_io.hpp:7-15, relation_io.cpp:48-103) -------
+
+def export_relation(rel: Relation, path) -> None:
+    """workloads::export_relation: manifest.txt + one raw little-endian file per
+    column (key.bin, payload<c>.bin).  Device columns are downloaded; numpy
+    columns are written as they are.  Readable by the reference's
+    import_relation and by import_relation below."""
+    import os
+    os.makedirs(path, exist_ok=True)
+
+    def host(c):
+        return np.ascontiguousarray(c) if isinstance(c, np.ndarray) else to_host(c)
+
+    cols = [("key", "key.bin", host(rel.key))] + \
+        [(f"payload{i}", f"payload{i}.bin", host(p)) for i, p in enumerate(rel.payloads)]
+    lines = [f"name {rel.name or 'relation'}", f"rows {len(cols[0][2])}",
+             f"key_unique {1 if rel.key_unique else 0}"]
+    for label, fname, a in cols:
+        if a.dtype.itemsize not in (4, 8):
+            raise A.SchemaError("columns are u32 or u64")
+        a.astype("<u4" if a.dtype.itemsize == 4 else "<u8", copy=False).tofile(
+            os.path.join(path, fname))
+        lines.append(f"column {label} {'u32' if a.dtype.itemsize == 4 else 'u64'} {fname}")
+    with open(os.path.join(path, "manifest.txt"), "w") as f:
+        f.write("\n".join(lines) + "\n")
+
+
+def import_relation(path, ctx: Optional[Context] = None) -> Relation:
+    """workloads::import_relation.  With a ctx the columns go straight to the
+    device (int32/int64 tensors holding the bits), else they stay numpy.
+    SchemaError on a missing/malformed manifest or a short column file."""
+    import os
+    mf = os.path.join(path, "manifest.txt")
+    if not os.path.exists(mf):
+        raise A.SchemaError(f"no manifest.txt in {path}")
+    name, rows, unique, key, pays = "", 0, False, None, []
+    with open(mf) as f:
+        for line in f:
+            line = line.rstrip("\n")
+            if not line or line.startswith("#"):
+                continue
+            tok = line.split()
+            if tok[0] == "name":
+                name = tok[1] if len(tok) > 1 else ""
+            elif tok[0] == "rows":
+                rows = int(tok[1])
+            elif tok[0] == "key_unique":
+                unique = int(tok[1]) != 0
+            elif tok[0] == "column":
+                if len(tok) < 4:
+                    raise A.SchemaError(f"malformed column line: {line}")
+                if tok[2] not in ("u32", "u64"):
+                    raise A.SchemaError(f"unknown column kind in manifest: {tok[2]}")
+                dt = np.dtype("<u4" if tok[2] == "u32" else "<u8")
+                a = np.fromfile(os.path.join(path, tok[3]), dtype=dt, count=rows)
+                if len(a) != rows:
+                    raise A.SchemaError(f"column file shorter than the manifest row count: {tok[3]}")
+                if tok[1] == "key":
+                    key = a
+                else:
+                    pays.append(a)
+            else:
+                raise A.SchemaError(f"unknown manifest field: {tok[0]}")
+    if key is None:
+        raise A.SchemaError("manifest lists no key column")
+    if ctx is not None:
+        key, pays = to_device(key), [to_device(p) for p in pays]
+    return Relation(key, pays, name, unique)

@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "cj_api.h"
@@ -35,6 +36,9 @@ struct cj_ctx {
   uint16_t epoch = 0;             // look-back status generation (see radix.cu)
   uint64_t launches = 0;          // kernels launched through this ctx
   uint64_t scratch_now = 0, scratch_peak = 0;  // device scratch held by operators
+  // every live alloc() of this ctx (bytes), for run_join's per-phase peaks
+  std::unordered_map<void*, uint64_t> live_sizes;
+  uint64_t live = 0, live_peak = 0;
   std::string last_error;
   // persistent scratch (grown on demand, never shrunk)
   uint64_t* status = nullptr;     // decoupled look-back words

@@ -278,6 +278,20 @@ void free_output(cj_ctx* ctx, cj_join_result* res) {
   res->ids_r = res->ids_s = nullptr;
 }
 
+// Device bytes this call holds (outputs, transformed columns, scratch) at
+// their high-water mark in each phase — PhaseReport's per-phase peaks
+// (mem_ledger.hpp:231-246) measured on the device arena instead of a ledger.
+struct PhasePeaks {
+  cj_ctx* ctx;
+  uint64_t base;
+  explicit PhasePeaks(cj_ctx* c) : ctx(c), base(c->live) { c->live_peak = c->live; }
+  uint64_t next() {  // peak since the last call; starts the next phase
+    const uint64_t p = ctx->live_peak > base ? ctx->live_peak - base : 0;
+    ctx->live_peak = ctx->live;
+    return p;
+  }
+};
+
 void run_join_dev(cj_ctx* ctx, const cj_relation* R, const cj_relation* S,
                   const cj_join_options* opt, cj_join_result* res) {
   validate_relation(R, "a build relation");
@@ -315,10 +329,12 @@ void run_join_dev(cj_ctx* ctx, const cj_relation* R, const cj_relation* S,
     }
   } guard{ctx, &owned};
 
+  PhasePeaks peaks(ctx);
   if (opt->algo == CJ_NPHJ) {
     // No transform: the build relation is hashed as is (nphj.cu).
     tm.mark(0);
     tm.mark(1);
+    res->peak_transform_b = peaks.next();
     OutSpec o;
     uint64_t cap = pk_fk ? S->rows : nphj_find(ctx, R->key, R->rows, S->key, S->rows, kb, o, 0, true);
     alloc_output(ctx, R, S, cap, true, res);
@@ -356,6 +372,7 @@ void run_join_dev(cj_ctx* ctx, const cj_relation* R, const cj_relation* S,
       total = nphj_find(ctx, R->key, R->rows, S->key, S->rows, kb, o, cap, false);
     }
     tm.mark(2);
+    res->peak_find_b = peaks.next();
     if (gfur) {
       const void* in[2 * CJ_MAX_COLS];
       void* out[2 * CJ_MAX_COLS];
@@ -374,6 +391,9 @@ void run_join_dev(cj_ctx* ctx, const cj_relation* R, const cj_relation* S,
       gather_cols(ctx, in, S->rows, res->ids_s, total, out, by, (int)S->npay);
     }
     tm.mark(3);
+    res->peak_materialize_b = peaks.next();
+    res->device_bytes_peak =
+        std::max({res->peak_transform_b, res->peak_find_b, res->peak_materialize_b});
     CJ_CUDA(cudaStreamSynchronize(ctx->stream));
     raise_device_errors(ctx);
     res->rows = total;
@@ -397,6 +417,7 @@ void run_join_dev(cj_ctx* ctx, const cj_relation* R, const cj_relation* S,
   Side tr = transform(ctx, R, opt->algo, gfur, total_bits, opt->radix_bits_per_pass, owned);
   Side ts = transform(ctx, S, opt->algo, gfur, total_bits, opt->radix_bits_per_pass, owned);
   tm.mark(1);
+  res->peak_transform_b = peaks.next();
 
   // ---- find (+ fused materialise for GFTR) ------------------------------------
   if (opt->algo == CJ_SMJ && opt->validate) {
@@ -466,6 +487,7 @@ void run_join_dev(cj_ctx* ctx, const cj_relation* R, const cj_relation* S,
     ctx->set_bytes(opt->algo == CJ_SMJ ? "smj_find" : "phj_find", b);
   }
   tm.mark(2);
+  res->peak_find_b = peaks.next();
 
   // ---- materialise (GFUR: gathers from the untransformed relations) -------
   if (gfur) {
@@ -486,6 +508,10 @@ void run_join_dev(cj_ctx* ctx, const cj_relation* R, const cj_relation* S,
     gather_cols(ctx, in, S->rows, res->ids_s, total, out, by, (int)S->npay);
   }
   tm.mark(3);
+  // the transformed columns are still held here (released with `owned`)
+  res->peak_materialize_b = peaks.next();
+  res->device_bytes_peak =
+      std::max({res->peak_transform_b, res->peak_find_b, res->peak_materialize_b});
   CJ_CUDA(cudaStreamSynchronize(ctx->stream));
   raise_device_errors(ctx);
   res->rows = total;
@@ -529,11 +555,20 @@ int guarded(cj_ctx* ctx, F&& fn) {
 void* cj_ctx::alloc(uint64_t bytes) {
   void* p = nullptr;
   cj::check_cuda(cudaMallocFromPoolAsync(&p, bytes ? bytes : 16, pool, stream), "cudaMallocAsync");
+  live_sizes[p] = bytes;
+  live += bytes;
+  live_peak = std::max(live_peak, live);
   return p;
 }
 
 void cj_ctx::release(void* p) {
-  if (p) cudaFreeAsync(p, stream);
+  if (!p) return;
+  auto it = live_sizes.find(p);
+  if (it != live_sizes.end()) {
+    live -= it->second;
+    live_sizes.erase(it);
+  }
+  cudaFreeAsync(p, stream);
 }
 
 uint16_t cj_ctx::next_epoch() {

@@ -739,6 +739,9 @@ JoinOutput run_join(const JoinTask& task) {
   out.report.transform_ns = res.transform_ns;
   out.report.find_ns = res.find_ns;
   out.report.materialize_ns = res.materialize_ns;
+  out.report.peak_by_phase[0].total_bytes = res.peak_transform_b;
+  out.report.peak_by_phase[1].total_bytes = res.peak_find_b;
+  out.report.peak_by_phase[2].total_bytes = res.peak_materialize_b;
   out.stats.matches = res.rows;
   out.stats.clusteredness_r = res.clusteredness_r;
   out.stats.clusteredness_s = res.clusteredness_s;
