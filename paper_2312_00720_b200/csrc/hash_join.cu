@@ -439,12 +439,12 @@ __global__ void k_phj_desc(const uint64_t* __restrict__ boff, const uint64_t* __
 
 // Rows [0, cnt) of a unit's output at ubase, column by column, consecutive
 // threads on consecutive output rows: row t is (build idx, probe idx) =
-// (me[t], t) when ident, else list[t] = build idx << 16 | probe idx.
+// (me[t] or res[t], t) when ident, else list[t] = build idx << 16 | probe idx.
 template <class K>
 __device__ __forceinline__ void emit_rows(const FindArgs& a, const UnitDesc& inf,
                                           const uint8_t* st, const K* pk, const uint16_t* me,
-                                          const uint32_t* list, uint64_t ubase, uint32_t cnt,
-                                          bool ident) {
+                                          const uint32_t* res, const uint32_t* list,
+                                          uint64_t ubase, uint32_t cnt, bool ident) {
   const int tid = threadIdx.x;
   const uint32_t bsh4 = (uint32_t)(inf.b_lo & 3), bsh8 = (uint32_t)(inf.b_lo & 1);
   const uint32_t qsh4 = (uint32_t)(inf.q_lo & 3), qsh8 = (uint32_t)(inf.q_lo & 1);
@@ -456,7 +456,7 @@ __device__ __forceinline__ void emit_rows(const FindArgs& a, const UnitDesc& inf
 #pragma unroll
     for (int k = 0; k < kE; ++k) {
       const uint32_t t = t0 + tid + k * kTmaThreads;
-      L[k] = t < cnt ? (ident ? ((uint32_t)me[t] << 16) | t : list[t]) : 0u;
+      L[k] = t < cnt ? (ident ? ((me ? (uint32_t)me[t] : res[t]) << 16) | t : list[t]) : 0u;
     }
     auto each = [&](auto&& f) {
 #pragma unroll
@@ -517,9 +517,10 @@ __device__ __forceinline__ void emit_compact(const FindArgs& a, const UnitDesc& 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t ubase = s_wbase[0];
   uint32_t cnt = (uint32_t)(s_wbase[kTmaWarps - 1] - ubase + s_wcount[kTmaWarps - 1]);
-  // every probe row matched once (PK-FK, match ratio 1): output row t is probe
-  // row t, its build row is me[t]; no compaction needed
-  const bool ident = me != nullptr && cnt == nq;
+  // every probe row matched once (PK-FK, match ratio 1; units without
+  // duplicate build keys): output row t is probe row t, its build row is me[t]
+  // (or res[t]); no compaction needed
+  const bool ident = cnt == nq;
   if (!ident) {
     // 3a. compact the hits in probe order: list[t] = (build idx << 16) | probe idx
     uint32_t o = (uint32_t)(s_wbase[warp] - ubase);
@@ -534,7 +535,7 @@ __device__ __forceinline__ void emit_compact(const FindArgs& a, const UnitDesc& 
     }
     __syncthreads();
   }
-  emit_rows<K>(a, inf, st, pk, me, list, ubase, cnt, ident);
+  emit_rows<K>(a, inf, st, pk, me, res, list, ubase, cnt, ident);
 }
 
 template <class K, bool WRITE>
@@ -586,7 +587,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constan
   // or skewed probe partition) follow each other and reuse the build table;
   // the single-pass look-back mode needs units in flight in global order
   // (round robin).
-  const bool blocked = !(WRITE && a.unit_off == nullptr) && a.np_rows > 0 && a.blocked;
+  const bool lookback = WRITE && a.unit_off == nullptr;
+  const bool blocked = !lookback && a.np_rows > 0 && a.blocked;
   // blocked ranges split the probe rows evenly (unit q_lo is monotone): units
   // differ in size (a skewed partition's full chunks vs small ones)
   auto first_unit = [&](uint64_t c) -> uint64_t {  // first unit with q_lo >= c * |S| / grid
@@ -663,7 +665,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constan
       dev::mbar_wait(&mbar[b], phase[b]);
       phase[b] ^= 1;
       if (ucnt == nq) {
-        emit_rows<K>(a, inf, st, pk, me, nullptr, ubase, nq, true);
+        emit_rows<K>(a, inf, st, pk, me, nullptr, nullptr, ubase, nq, true);
         __syncthreads();
         if (a.stages == 1 && tid == 0) issue_next(0);
         continue;
@@ -784,7 +786,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constan
       const uint64_t wc = lane < kTmaWarps ? s_wcount[lane] : 0;
       const uint64_t inc = dev::warp_inclusive_sum(wc);
       uint64_t base;
-      if (WRITE && a.unit_off == nullptr) {
+      if (lookback) {
         // single pass: the unit's output offset by decoupled look-back over
         // the units in order (every CTA is resident; units are taken in order)
         const uint64_t tot = __shfl_sync(0xffffffffu, inc, kTmaWarps - 1);
