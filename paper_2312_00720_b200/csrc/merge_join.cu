@@ -460,18 +460,29 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_smj_tma(const __grid_constan
       }
     } else if (win) {
       uint32_t lb = 0;
+      uint16_t e16[kSmjPer];
 #pragma unroll
       for (uint32_t q = 0; q < kSmjPer; ++q) {
         const uint32_t jl = j0 + q;
+        e16[q] = 0xffffu;
         if (jl < nq) {
           const K k = sk[jl];
           if (q == 0) {
-            uint32_t lo = 0, hi = (uint32_t)w;
-            while (lo < hi) {
-              const uint32_t mid = (lo + hi) >> 1;
-              if (rk[mid] < k) lo = mid + 1; else hi = mid;
+            // interpolate between the window's end keys (exact on dense
+            // keys), then gallop to the lower bound from below
+            uint32_t g = 0;
+            const K r0 = w ? rk[0] : K(0), r1 = w ? rk[w - 1] : K(0);
+            if (w > 1 && k > r0 && r1 > r0) {
+              const float f = (float)(k - r0) / (float)(r1 - r0);
+              g = (uint32_t)fminf((float)(w - 1), f * (float)(w - 1));
+              // step back until rk[g] < k (or g = 0) so galloping stays monotone
+              uint32_t back = 1;
+              while (g > 0 && !(rk[g] < k)) {
+                g = g > back ? g - back : 0;
+                back <<= 1;
+              }
             }
-            lb = lo;
+            lb = gallop<K, false>(rk, g, (uint32_t)w, k);
           } else {
             lb = gallop<K, false>(rk, lb, (uint32_t)w, k);
           }
@@ -480,8 +491,15 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_smj_tma(const __grid_constan
           loff[jl] = lb;
           mcnt[jl] = m;
           tsum += m;
-          if (!WRITE && a.match_e) a.match_e[d.s_lo + jl] = (uint16_t)(m ? lb : 0xffffu);
+          e16[q] = (uint16_t)(m ? lb : 0xffffu);
         }
+      }
+      if (!WRITE && a.match_e) {  // four u16 hand-off entries in one 8-byte store
+        if (j0 + kSmjPer <= nq)
+          *reinterpret_cast<uint2*>(a.match_e + d.s_lo + j0) =
+              make_uint2(e16[0] | ((uint32_t)e16[1] << 16), e16[2] | ((uint32_t)e16[3] << 16));
+        else
+          for (uint32_t q = 0; q < kSmjPer && j0 + q < nq; ++q) a.match_e[d.s_lo + j0 + q] = e16[q];
       }
     } else {  // window beyond shared memory: global binary searches
 #pragma unroll
