@@ -916,8 +916,9 @@ bool tma_layout(FindArgs& a, size_t* smem_out) {
   }
   a.stage_bytes = (uint32_t)off;
   a.cap_entries = 1u << a.cap_log2;
-  // + res[qchunk] probe results + list[qchunk] compacted hits
-  const size_t smem = (size_t)a.stages * off + up(4 * (size_t)a.cap_entries) + (size_t)a.qchunk * 8;
+  // + res[qchunk] probe results + list[qchunk] compacted hits (fill only)
+  const size_t smem = (size_t)a.stages * off + up(4 * (size_t)a.cap_entries) +
+                      (a.write ? (size_t)a.qchunk * 8 : 0);
   *smem_out = smem;
   return smem <= 225 * 1024;  // + < 2 KB of static shared memory
 }
