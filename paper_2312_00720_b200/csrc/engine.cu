@@ -443,9 +443,17 @@ void run_join_dev(cj_ctx* ctx, const cj_relation* R, const cj_relation* S,
     o.r_rows = R->rows;
     o.s_rows = S->rows;
     if (gfur) {
-      o.ids_r = res->ids_r ? res->ids_r : nullptr;
-      o.carried_r = static_cast<const uint32_t*>(tr.cols[0]);
-      o.carried_s = static_cast<const uint32_t*>(ts.cols[0]);
+      // the physical ids carried through the transform are moved like a
+      // payload column (staged by the find's bulk copies, written at the
+      // output row) into ids_r / ids_s: resolve_ids (join_engine.cpp:37-45)
+      o.ids_r = o.ids_s = nullptr;
+      o.nr = o.ns = 1;
+      o.r_src[0] = tr.cols[0];
+      o.r_dst[0] = res->ids_r;
+      o.r_bytes[0] = 4;
+      o.s_src[0] = ts.cols[0];
+      o.s_dst[0] = res->ids_s;
+      o.s_bytes[0] = 4;
     } else {
       o.nr = (int)R->npay;
       o.ns = (int)S->npay;
@@ -482,8 +490,11 @@ void run_join_dev(cj_ctx* ctx, const cj_relation* R, const cj_relation* S,
       for (uint32_t c = 0; c < R->npay; ++c) rrow += R->pay_bytes[c];
       for (uint32_t c = 0; c < S->npay; ++c) srow += S->pay_bytes[c];
       out_row += rrow + srow - 2 * kb;
+    } else {  // the carried ids are read once, like a payload column
+      rrow += 4;
+      srow += 4;
     }
-    const uint64_t b = rrow * R->rows + srow * S->rows + out_row * total + (gfur ? 8 * total : 0);
+    const uint64_t b = rrow * R->rows + srow * S->rows + out_row * total;
     ctx->set_bytes(opt->algo == CJ_SMJ ? "smj_find" : "phj_find", b);
   }
   tm.mark(2);
