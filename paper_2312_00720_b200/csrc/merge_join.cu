@@ -341,83 +341,102 @@ __device__ __forceinline__ void smj_emit_rows(const SmjArgs& a, const SmjDesc& d
   }
 }
 
+// Warp-specialised: warp kTmaWarps (the producer) walks this CTA's tiles, reads
+// each tile's descriptor (and, in the fill, the count pass's total and offset)
+// into shared memory and bulk-copies the tile into a free stage; the 16
+// consumer warps take stages as their copies land (full barriers) and hand
+// them back per warp (empty barriers), so a warp that finishes a tile early
+// starts the next one instead of waiting for the slowest warp.  Consumer-wide
+// steps of the general path synchronise on named barrier 1 (512 threads).
+constexpr int kSmjStages = 2;
+
 template <class K, bool WRITE>
-__global__ void __launch_bounds__(kTmaThreads, 1) k_smj_tma(const __grid_constant__ SmjArgs a) {
+__global__ void __launch_bounds__(kTmaThreads + 32, 1) k_smj_tma(const __grid_constant__ SmjArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
-  uint32_t* loff = reinterpret_cast<uint32_t*>(smem + 2 * (size_t)a.stage_bytes);
+  uint32_t* loff = reinterpret_cast<uint32_t*>(smem + kSmjStages * (size_t)a.stage_bytes);
   uint32_t* mcnt = loff + kTileS;
   uint32_t* list = mcnt + kTileS;  // [kSmjList] (WRITE)
-  __shared__ SmjDesc s_desc[2];
-  __shared__ bool s_pre[2];
-  __shared__ __align__(8) uint64_t mbar[2];
-  __shared__ uint64_t s_wcount[kTmaWarps], s_wbase[kTmaWarps];
+  __shared__ SmjDesc s_desc[kSmjStages];
+  __shared__ bool s_pre[kSmjStages];
+  __shared__ uint64_t s_fcnt[kSmjStages], s_fbase[kSmjStages];
+  __shared__ __align__(8) uint64_t full[kSmjStages], empty[kSmjStages];
+  __shared__ uint64_t s_wcnt[2][kTmaWarps], s_wb[2][kTmaWarps];  // by tile parity
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const SmjDesc* __restrict__ descs = static_cast<const SmjDesc*>(a.desc);
   const K* __restrict__ rg = static_cast<const K*>(a.r);
   const uint32_t kb = sizeof(K);
+  const uint64_t g = gridDim.x;
   auto bytes = [&](uint64_t lo, uint64_t hi, uint32_t w) {
     return hi > lo ? (uint32_t)((dev::align_hi(hi, w) - dev::align_lo(lo, w)) * w) : 0u;
   };
-  auto is_pre = [&](uint64_t tt) { return WRITE && a.match_e != nullptr && a.tile_pre[tt] != 0; };
-  auto issue = [&](int b, const SmjDesc& d, bool pre) {  // thread 0
-    uint8_t* st = smem + (size_t)b * a.stage_bytes;
-    const bool win = d.r_hi - d.r_lo <= a.wmax;
-    uint32_t total = bytes(d.s_lo, d.s_hi, kb);
-    if (win && !pre) total += bytes(d.r_lo, d.r_hi, kb);
-    if (WRITE) {
-      if (win)
-        for (int c = 0; c < a.nr_cols; ++c) total += bytes(d.r_lo, d.r_hi, a.r_bytes[c]);
-      for (int c = 0; c < a.ns_cols; ++c) total += bytes(d.s_lo, d.s_hi, a.s_bytes[c]);
-      if (pre) total += bytes(d.s_lo, d.s_hi, 2);
-    }
-    dev::mbar_expect_tx(&mbar[b], total);
-    auto copy = [&](uint32_t off, const void* base, uint64_t lo, uint64_t hi, uint32_t w) {
-      if (hi > lo)
-        dev::tma_load_1d(st + off, static_cast<const uint8_t*>(base) + dev::align_lo(lo, w) * w,
-                         bytes(lo, hi, w), &mbar[b]);
-    };
-    copy(a.off_sk, a.s, d.s_lo, d.s_hi, kb);
-    if (win && !pre) copy(a.off_rk, a.r, d.r_lo, d.r_hi, kb);
-    if (WRITE) {
-      if (win)
-        for (int c = 0; c < a.nr_cols; ++c) copy(a.off_r[c], a.r_src[c], d.r_lo, d.r_hi, a.r_bytes[c]);
-      for (int c = 0; c < a.ns_cols; ++c) copy(a.off_s[c], a.s_src[c], d.s_lo, d.s_hi, a.s_bytes[c]);
-      if (pre) copy(a.off_e, a.match_e, d.s_lo, d.s_hi, 2);
-    }
-  };
-  uint64_t t = blockIdx.x;
-  SmjDesc next{};
-  bool next_pre = false;
   if (tid == 0) {
-    dev::mbar_init(&mbar[0], 1);
-    dev::mbar_init(&mbar[1], 1);
+    for (int i = 0; i < kSmjStages; ++i) {
+      dev::mbar_init(&full[i], 1);
+      dev::mbar_init(&empty[i], kTmaWarps);
+    }
     dev::fence_mbar_init();
-    if (t < a.tiles) {
-      s_desc[0] = descs[t];
-      s_pre[0] = is_pre(t);
-      issue(0, s_desc[0], s_pre[0]);
-    }
-    if (t + gridDim.x < a.tiles) {
-      next = descs[t + gridDim.x];
-      next_pre = is_pre(t + gridDim.x);
-    }
   }
   __syncthreads();
-  uint32_t phase[2] = {0, 0};
-  int b = 0;
-  for (; t < a.tiles; t += gridDim.x, b ^= 1) {
-    const SmjDesc d = s_desc[b];
-    const bool pre = s_pre[b];
-    if (tid == 0 && t + gridDim.x < a.tiles) {
-      s_desc[b ^ 1] = next;
-      s_pre[b ^ 1] = next_pre;
+
+  if (warp == kTmaWarps) {  // ---- producer ----
+    if (lane != 0) return;
+    uint32_t k = 0;
+    for (uint64_t t = blockIdx.x; t < a.tiles; t += g, ++k) {
+      const int b = (int)(k % kSmjStages);
+      if (k >= kSmjStages) dev::mbar_wait(&empty[b], ((k / kSmjStages) - 1) & 1u);
+      const SmjDesc d = descs[t];
+      const bool pre = WRITE && a.match_e != nullptr && a.tile_pre[t] != 0;
+      s_desc[b] = d;
+      s_pre[b] = pre;
+      if (WRITE) {
+        const bool f = pre && a.tile_counts != nullptr;
+        s_fcnt[b] = f ? a.tile_counts[t] : ~0ull;
+        s_fbase[b] = f ? a.tile_off[t] : 0;
+      }
+      uint8_t* st = smem + (size_t)b * a.stage_bytes;
+      const bool win = d.r_hi - d.r_lo <= a.wmax;
+      uint32_t total = bytes(d.s_lo, d.s_hi, kb);
+      if (win && !pre) total += bytes(d.r_lo, d.r_hi, kb);
+      if (WRITE) {
+        if (win)
+          for (int c = 0; c < a.nr_cols; ++c) total += bytes(d.r_lo, d.r_hi, a.r_bytes[c]);
+        for (int c = 0; c < a.ns_cols; ++c) total += bytes(d.s_lo, d.s_hi, a.s_bytes[c]);
+        if (pre) total += bytes(d.s_lo, d.s_hi, 2);
+      }
       dev::fence_proxy_async();
-      issue(b ^ 1, next, next_pre);
-      if (t + 2ull * gridDim.x < a.tiles) {
-        next = descs[t + 2ull * gridDim.x];
-        next_pre = is_pre(t + 2ull * gridDim.x);
+      dev::mbar_expect_tx(&full[b], total);
+      auto copy = [&](uint32_t off, const void* base, uint64_t lo, uint64_t hi, uint32_t w) {
+        if (hi > lo)
+          dev::tma_load_1d(st + off, static_cast<const uint8_t*>(base) + dev::align_lo(lo, w) * w,
+                           bytes(lo, hi, w), &full[b]);
+      };
+      copy(a.off_sk, a.s, d.s_lo, d.s_hi, kb);
+      if (win && !pre) copy(a.off_rk, a.r, d.r_lo, d.r_hi, kb);
+      if (WRITE) {
+        if (win)
+          for (int c = 0; c < a.nr_cols; ++c) copy(a.off_r[c], a.r_src[c], d.r_lo, d.r_hi, a.r_bytes[c]);
+        for (int c = 0; c < a.ns_cols; ++c) copy(a.off_s[c], a.s_src[c], d.s_lo, d.s_hi, a.s_bytes[c]);
+        if (pre) copy(a.off_e, a.match_e, d.s_lo, d.s_hi, 2);
       }
     }
+    return;
+  }
+
+  // ---- consumers ----
+  auto consumers_sync = [] { dev::named_bar(1, kTmaThreads); };
+  auto release = [&](int b) {  // this warp is done with stage b
+    __syncwarp();
+    if (lane == 0) dev::mbar_arrive(&empty[b]);
+  };
+  uint32_t k = 0;
+  for (uint64_t t = blockIdx.x; t < a.tiles; t += g, ++k) {
+    const int b = (int)(k % kSmjStages);
+    const int par = (int)(k & 1u);
+    uint64_t* s_wcount = s_wcnt[par];
+    uint64_t* s_wbase = s_wb[par];
+    dev::mbar_wait(&full[b], (k / kSmjStages) & 1u);
+    const SmjDesc d = s_desc[b];
+    const bool pre = s_pre[b];
     uint64_t tile_base = 0;
     if (WRITE && tid == 32) tile_base = a.tile_off[t];
     uint8_t* st = smem + (size_t)b * a.stage_bytes;
@@ -430,19 +449,15 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_smj_tma(const __grid_constan
     // r window is staged; the count pass may take wider windows) -> the
     // output rows are the probe rows in order, their r rows are match_e; no
     // bounds, scan or compaction
-    const bool fast_ok = WRITE && pre && win && a.tile_counts != nullptr;
-    const uint64_t fcnt = fast_ok ? a.tile_counts[t] : ~0ull;
-    const uint64_t fbase = fast_ok ? a.tile_off[t] : 0;
-    dev::mbar_wait(&mbar[b], phase[b]);
-    phase[b] ^= 1;
+    const uint64_t fcnt = WRITE && pre && win ? s_fcnt[b] : ~0ull;
     if (WRITE && fcnt == nq) {
       const uint16_t* me = reinterpret_cast<const uint16_t*>(st + a.off_e) +
                            (d.s_lo - dev::align_lo(d.s_lo, 2));
-      smj_emit_rows<K>(a, d, st, sk, fbase, nq, [&](uint32_t tt) { return ((uint32_t)me[tt] << 16) | tt; });
-      __syncthreads();
+      smj_emit_rows<K>(a, d, st, sk, s_fbase[b], nq,
+                       [&](uint32_t tt) { return ((uint32_t)me[tt] << 16) | tt; });
+      release(b);
       continue;
     }
-    __syncthreads();
 
     // 1. bounds of this thread's four probes
     const uint32_t j0 = tid * kSmjPer;
@@ -519,7 +534,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_smj_tma(const __grid_constan
     if (!WRITE && a.match_e && tid == 0) a.tile_pre[t] = (a.pk_fk && win) ? 1 : 0;
     const uint32_t tinc = dev::warp_inclusive_sum(tsum);
     if (lane == 31) s_wcount[warp] = tinc;
-    __syncthreads();
+    consumers_sync();
+    if (!WRITE) release(b);  // the count pass reads the stage no further
     if (warp == 1) {
       const uint64_t v = lane < kTmaWarps ? s_wcount[lane] : 0;
       const uint64_t inc = dev::warp_inclusive_sum(v);
@@ -528,7 +544,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_smj_tma(const __grid_constan
       if (!WRITE && lane == kTmaWarps - 1) a.tile_counts[t] = inc;
     }
     if (!WRITE) continue;
-    __syncthreads();
+    consumers_sync();
     const uint32_t ssh4 = (uint32_t)(d.s_lo & 3), ssh8 = (uint32_t)(d.s_lo & 1);
     const uint32_t rsh4 = (uint32_t)(d.r_lo & 3), rsh8 = (uint32_t)(d.r_lo & 1);
     const uint64_t tbase = s_wbase[0];
@@ -547,7 +563,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_smj_tma(const __grid_constan
             for (uint32_t i = 0; i < m; ++i) list[o++] = ((l0 + i) << 16) | jl;
           }
         }
-        __syncthreads();
+        consumers_sync();
       }
       // 2b. column by column, consecutive threads on consecutive output rows
       const uint32_t* lst = list;
@@ -557,7 +573,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_smj_tma(const __grid_constan
                          [&](uint32_t tt) { return (lof[tt] << 16) | tt; });
       else
         smj_emit_rows<K>(a, d, st, sk, tbase, (uint32_t)tcount, [&](uint32_t tt) { return lst[tt]; });
-      __syncthreads();
+      release(b);
+      consumers_sync();  // loff / mcnt / list are rewritten by the next tile
       continue;
     }
     // general: per probe, its whole r run (probe rows in rounds of 32)
@@ -602,7 +619,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_smj_tma(const __grid_constan
       }
       o += __shfl_sync(0xffffffffu, inc, 31);
     }
-    __syncthreads();
+    release(b);
+    consumers_sync();
   }
 }
 
@@ -675,12 +693,12 @@ uint64_t run_tma(cj_ctx* ctx, SmjArgs a) {
   CJ_CUDA(cudaFuncSetAttribute(k_smj_tma<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem_c));
   int per_sm = 1;
-  CJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_smj_tma<K, false>, kTmaThreads,
+  CJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_smj_tma<K, false>, kTmaThreads + 32,
                                                         smem_c));
   const unsigned grid_c = (unsigned)std::min<uint64_t>(
       (uint64_t)ctx->num_sms * std::max(1, std::min(per_sm, 2)), a.tiles);
   ctx->kbegin("smj_count", sizeof(K) * (a.nr + a.ns));
-  k_smj_tma<K, false><<<grid_c, kTmaThreads, smem_c, ctx->stream>>>(ac);
+  k_smj_tma<K, false><<<grid_c, kTmaThreads + 32, smem_c, ctx->stream>>>(ac);
   ctx->kend();
   scan_counts(ctx, counts.as<uint64_t>(), a.tiles, offs.as<uint64_t>(), tot.as<uint64_t>());
   CJ_CUDA(cudaGetLastError());
@@ -695,7 +713,7 @@ uint64_t run_tma(cj_ctx* ctx, SmjArgs a) {
     CJ_CUDA(cudaFuncSetAttribute(k_smj_tma<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
     ctx->kbegin("smj_find", 0);
-    k_smj_tma<K, true><<<grid, kTmaThreads, smem, ctx->stream>>>(a);
+    k_smj_tma<K, true><<<grid, kTmaThreads + 32, smem, ctx->stream>>>(a);
     ctx->kend();
     CJ_CUDA(cudaGetLastError());
   }
