@@ -533,54 +533,36 @@ __device__ __forceinline__ void emit_compact(const FindArgs& a, const UnitDesc& 
       if (hit) list[o + __popc(bal & dev::lanemask_lt())] = (e << 16) | jl;
       o += __popc(bal);
     }
-    __syncthreads();
+    dev::named_bar(1, kTmaThreads);  // the consumer warps of k_phj_tma
   }
   emit_rows<K>(a, inf, st, pk, me, res, list, ubase, cnt, ident);
 }
 
+// Warp-specialised like k_smj_tma: warp kTmaWarps (the producer) walks this
+// CTA's units, puts each unit's descriptor (and, in the fill, the count pass's
+// total and offset) in shared memory and bulk-copies its columns into a free
+// stage; the 16 consumer warps take stages as the copies land (full barriers)
+// and hand them back per warp (empty barriers).  Units the count pass fully
+// resolved (the PK-FK fill) need no consumer-wide barrier at all; the other
+// paths synchronise the consumers on named barrier 1.
 template <class K, bool WRITE>
-__global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constant__ FindArgs a) {
+__global__ void __launch_bounds__(kTmaThreads + 32, WRITE ? 1 : 2)
+k_phj_tma(const __grid_constant__ FindArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint32_t* tab = reinterpret_cast<uint32_t*>(smem + (size_t)a.stages * a.stage_bytes);
   uint32_t* res = tab + a.cap_entries;
   __shared__ UnitDesc s_desc[2];
   __shared__ bool s_pre[2];
-  __shared__ __align__(8) uint64_t mbar[2];
-  __shared__ uint64_t s_wcount[kTmaWarps], s_wbase[kTmaWarps];
+  __shared__ uint64_t s_ucnt[2], s_ubase[2];
+  __shared__ __align__(8) uint64_t full[2], empty[2];
+  __shared__ uint64_t s_wcnt[2][kTmaWarps], s_wb[2][kTmaWarps];  // by unit parity
   __shared__ int s_dup;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t units = a.n_units;
   const UnitDesc* __restrict__ descs = reinterpret_cast<const UnitDesc*>(a.desc);
   const uint32_t kb = sizeof(K);
-
-  auto bytes = [&](uint64_t lo, uint64_t hi, uint32_t w) {
-    return (uint32_t)((dev::align_hi(hi, w) - dev::align_lo(lo, w)) * w);
-  };
-  // pre: the count pass resolved this unit's matches (match_e); no build keys needed
-  auto issue = [&](int b, const UnitDesc& d, bool pre) {  // thread 0
-    uint8_t* st = smem + (size_t)b * a.stage_bytes;
-    uint32_t total = bytes(d.q_lo, d.q_hi, kb);
-    if (!pre) total += bytes(d.b_lo, d.b_hi, kb);
-    if (WRITE) {
-      for (int c = 0; c < a.nr; ++c) total += bytes(d.b_lo, d.b_hi, a.r_bytes[c]);
-      for (int c = 0; c < a.ns; ++c) total += bytes(d.q_lo, d.q_hi, a.s_bytes[c]);
-      if (pre) total += bytes(d.q_lo, d.q_hi, 2);
-    }
-    dev::mbar_expect_tx(&mbar[b], total);
-    auto copy = [&](uint32_t off, const void* base, uint64_t lo, uint64_t hi, uint32_t w) {
-      dev::tma_load_1d(st + off, static_cast<const uint8_t*>(base) + dev::align_lo(lo, w) * w,
-                       bytes(lo, hi, w), &mbar[b]);
-    };
-    if (!pre) copy(a.off_bk, a.bkeys, d.b_lo, d.b_hi, kb);
-    copy(a.off_pk, a.pkeys, d.q_lo, d.q_hi, kb);
-    if (WRITE) {
-      for (int c = 0; c < a.nr; ++c) copy(a.off_r[c], a.r_src[c], d.b_lo, d.b_hi, a.r_bytes[c]);
-      for (int c = 0; c < a.ns; ++c) copy(a.off_s[c], a.s_src[c], d.q_lo, d.q_hi, a.s_bytes[c]);
-      if (pre) copy(a.off_e, a.match_e, d.q_lo, d.q_hi, 2);
-    }
-  };
-  auto is_pre = [&](uint64_t uu) { return WRITE && a.match_e != nullptr && a.unit_dup[uu] == 0; };
+  const int S = a.stages;
 
   // Unit order: with precomputed unit offsets (two passes) each CTA walks a
   // contiguous range of units, so the probe chunks of one build chunk (a large
@@ -600,52 +582,86 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constan
     }
     return lo;
   };
-  const uint64_t u_end = blocked ? (blockIdx.x + 1 == gridDim.x ? units : first_unit(blockIdx.x + 1))
-                                 : units;
-  const uint64_t step = blocked ? 1 : gridDim.x;
-  uint64_t u = blocked ? (blockIdx.x == 0 ? 0 : first_unit(blockIdx.x)) : blockIdx.x;
-  UnitDesc next{};  // descriptor of the unit after the one in flight (thread 0)
-  bool next_pre = false;
+  const bool producer = warp == kTmaWarps;
+  uint64_t u_begin = 0, u_end = units;
   if (tid == 0) {
-    dev::mbar_init(&mbar[0], 1);
-    dev::mbar_init(&mbar[1], 1);
+    u_end = blocked ? (blockIdx.x + 1 == gridDim.x ? units : first_unit(blockIdx.x + 1)) : units;
+    u_begin = blocked ? (blockIdx.x == 0 ? 0 : first_unit(blockIdx.x)) : blockIdx.x;
+  }
+  __shared__ uint64_t s_range[2];
+  if (tid == 0) {
+    s_range[0] = u_begin;
+    s_range[1] = u_end;
+    for (int i = 0; i < 2; ++i) {
+      dev::mbar_init(&full[i], 1);
+      dev::mbar_init(&empty[i], kTmaWarps);
+    }
     dev::fence_mbar_init();
-    if (u < u_end) {
-      s_desc[0] = descs[u];
-      s_pre[0] = is_pre(u);
-      issue(0, s_desc[0], s_pre[0]);
-    }
-    if (u + step < u_end) {
-      next = descs[u + step];
-      next_pre = is_pre(u + step);
-    }
   }
   __syncthreads();
-  uint32_t phase[2] = {0, 0};
-  int b = 0;
-  auto issue_next = [&](int nb_) {  // thread 0: copies of unit u + step into stage nb_
-    if (u + step < u_end) {
-      s_desc[nb_] = next;
-      s_pre[nb_] = next_pre;
+  u_begin = s_range[0];
+  u_end = s_range[1];
+  const uint64_t step = blocked ? 1 : gridDim.x;
+
+  if (producer) {  // ---- producer (one thread) ----
+    if (lane != 0) return;
+    auto bytes = [&](uint64_t lo, uint64_t hi, uint32_t w) {
+      return (uint32_t)((dev::align_hi(hi, w) - dev::align_lo(lo, w)) * w);
+    };
+    uint32_t k = 0;
+    for (uint64_t u = u_begin; u < u_end; u += step, ++k) {
+      const int b = (int)(k % (uint32_t)S);
+      if (k >= (uint32_t)S) dev::mbar_wait(&empty[b], ((k / S) - 1) & 1u);
+      const UnitDesc d = descs[u];
+      // pre: the count pass resolved this unit's matches (match_e); no build keys needed
+      const bool pre = WRITE && a.match_e != nullptr && a.unit_dup[u] == 0;
+      s_desc[b] = d;
+      s_pre[b] = pre;
+      if (WRITE) {
+        s_ucnt[b] = pre && a.unit_counts ? a.unit_counts[u] : ~0ull;
+        s_ubase[b] = a.unit_off ? a.unit_off[u] : 0;
+      }
+      uint8_t* st = smem + (size_t)b * a.stage_bytes;
+      uint32_t total = bytes(d.q_lo, d.q_hi, kb);
+      if (!pre) total += bytes(d.b_lo, d.b_hi, kb);
+      if (WRITE) {
+        for (int c = 0; c < a.nr; ++c) total += bytes(d.b_lo, d.b_hi, a.r_bytes[c]);
+        for (int c = 0; c < a.ns; ++c) total += bytes(d.q_lo, d.q_hi, a.s_bytes[c]);
+        if (pre) total += bytes(d.q_lo, d.q_hi, 2);
+      }
       dev::fence_proxy_async();
-      issue(nb_, next, next_pre);
-      if (u + 2 * step < u_end) {  // in flight
-        next = descs[u + 2 * step];
-        next_pre = is_pre(u + 2 * step);
+      dev::mbar_expect_tx(&full[b], total);
+      auto copy = [&](uint32_t off, const void* base, uint64_t lo, uint64_t hi, uint32_t w) {
+        dev::tma_load_1d(st + off, static_cast<const uint8_t*>(base) + dev::align_lo(lo, w) * w,
+                         bytes(lo, hi, w), &full[b]);
+      };
+      if (!pre) copy(a.off_bk, a.bkeys, d.b_lo, d.b_hi, kb);
+      copy(a.off_pk, a.pkeys, d.q_lo, d.q_hi, kb);
+      if (WRITE) {
+        for (int c = 0; c < a.nr; ++c) copy(a.off_r[c], a.r_src[c], d.b_lo, d.b_hi, a.r_bytes[c]);
+        for (int c = 0; c < a.ns; ++c) copy(a.off_s[c], a.s_src[c], d.q_lo, d.q_hi, a.s_bytes[c]);
+        if (pre) copy(a.off_e, a.match_e, d.q_lo, d.q_hi, 2);
       }
     }
+    return;
+  }
+
+  // ---- consumers ----
+  auto sync_c = [] { dev::named_bar(1, kTmaThreads); };
+  auto release = [&](int b) {  // this warp is done with stage b
+    __syncwarp();
+    if (lane == 0) dev::mbar_arrive(&empty[b]);
   };
   uint64_t built_lo = ~0ull, built_hi = 0;  // build chunk whose table is in shared memory
-  for (; u < u_end; u += step, b = (b + 1) % a.stages) {
+  uint32_t k = 0;
+  for (uint64_t u = u_begin; u < u_end; u += step, ++k) {
+    const int b = (int)(k % (uint32_t)S);
+    uint64_t* s_wcount = s_wcnt[k & 1u];
+    uint64_t* s_wbase = s_wb[k & 1u];
+    dev::mbar_wait(&full[b], (k / S) & 1u);
     const UnitDesc inf = s_desc[b];
     const bool pre = s_pre[b];
     const bool reuse = inf.b_lo == built_lo && inf.b_hi == built_hi;
-    if (tid == 0) {
-      if (a.stages == 2) issue_next(b ^ 1);
-      if (!reuse) s_dup = 0;
-    }
-    uint64_t unit_base = 0;
-    if (WRITE && tid == 32 && a.unit_off) unit_base = a.unit_off[u];
     const uint32_t nb = (uint32_t)(inf.b_hi - inf.b_lo), nq = (uint32_t)(inf.q_hi - inf.q_lo);
     uint8_t* st = smem + (size_t)b * a.stage_bytes;
     const K* bk = reinterpret_cast<const K*>(st + a.off_bk) + (inf.b_lo - dev::align_lo(inf.b_lo, kb));
@@ -654,20 +670,15 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constan
     const uint32_t r0 = (uint32_t)((uint64_t)rounds * warp / kTmaWarps);
     const uint32_t r1 = (uint32_t)((uint64_t)rounds * (warp + 1) / kTmaWarps);
     if (pre) {
-      // matches resolved by the count pass: count this warp's hits, then
-      // continue at the compaction below (res <- match_e)
+      // matches resolved by the count pass
       const uint16_t* me = reinterpret_cast<const uint16_t*>(st + a.off_e) +
                            (inf.q_lo - dev::align_lo(inf.q_lo, 2));
-      // the count pass's per-unit total: every probe row matched once -> the
-      // output rows are the probe rows in order, no count / scan / compaction
-      const uint64_t ucnt = a.unit_counts ? a.unit_counts[u] : ~0ull;
-      const uint64_t ubase = a.unit_counts ? a.unit_off[u] : 0;
-      dev::mbar_wait(&mbar[b], phase[b]);
-      phase[b] ^= 1;
-      if (ucnt == nq) {
+      const uint64_t ubase = s_ubase[b];
+      if (s_ucnt[b] == nq) {
+        // every probe row matched once: the output rows are the probe rows in
+        // order; no count, scan or compaction, no consumer-wide barrier
         emit_rows<K>(a, inf, st, pk, me, nullptr, nullptr, ubase, nq, true);
-        __syncthreads();
-        if (a.stages == 1 && tid == 0) issue_next(0);
+        release(b);
         continue;
       }
       uint64_t wc = 0;
@@ -677,27 +688,26 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constan
         wc += __popc(__ballot_sync(0xffffffffu, hit));
       }
       if (lane == 0) s_wcount[warp] = wc;
-      __syncthreads();
+      sync_c();
       if (warp == 1) {
         const uint64_t c = lane < kTmaWarps ? s_wcount[lane] : 0;
         const uint64_t inc = dev::warp_inclusive_sum(c);
-        const uint64_t base = __shfl_sync(0xffffffffu, unit_base, 0);
-        if (lane < kTmaWarps) s_wbase[lane] = base + inc - c;
+        if (lane < kTmaWarps) s_wbase[lane] = ubase + inc - c;
       }
-      __syncthreads();
+      sync_c();
       emit_compact<K>(a, inf, st, pk, me, nullptr, r0, r1, nq, s_wbase, s_wcount, res + a.qchunk);
-      __syncthreads();
-      if (a.stages == 1 && tid == 0) issue_next(0);
+      release(b);
+      sync_c();  // res / list are rewritten by the next unit
       continue;
     }
     uint32_t cap_log2 = 1;
     while ((1u << cap_log2) < 2 * nb) ++cap_log2;
     const uint32_t cap = 1u << cap_log2, cmask = cap - 1;
-    if (!reuse)
+    if (!reuse) {
+      if (tid == 0) s_dup = 0;
       for (uint32_t i = tid; i < cap; i += kTmaThreads) tab[i] = kNoMatch;
-    dev::mbar_wait(&mbar[b], phase[b]);
-    phase[b] ^= 1;
-    __syncthreads();
+    }
+    sync_c();
 
     // 1. insert chunk positions (CAS); meeting an equal key marks duplicates
     //    (a plain-store first round measured slower: profiles/r01b_summary.md).
@@ -705,17 +715,17 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constan
     //    its sorted positions) in shared memory: reuse it.
     bool dup = false;
     for (uint32_t i = reuse ? nb : tid; i < nb; i += kTmaThreads) {
-      const K k = bk[i];
-      uint32_t sl = slot_of(k, cap_log2);
+      const K key = bk[i];
+      uint32_t sl = slot_of(key, cap_log2);
       while (true) {
         const uint32_t old = atomicCAS(&tab[sl], kNoMatch, i);
         if (old == kNoMatch) break;
-        if (bk[old] == k) dup = true;
+        if (bk[old] == key) dup = true;
         sl = (sl + 1) & cmask;
       }
     }
-    if (__syncthreads_or(dup)) s_dup = 1;
-    __syncthreads();
+    if (dev::named_bar_or(1, kTmaThreads, dup)) s_dup = 1;
+    sync_c();
     const bool has_dup = s_dup != 0;
     if (!WRITE && a.unit_dup && tid == 0) a.unit_dup[u] = has_dup ? 1 : 0;
     uint16_t* sidx = reinterpret_cast<uint16_t*>(tab);
@@ -725,7 +735,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constan
       uint32_t np2 = 1;
       while (np2 < nb) np2 <<= 1;
       for (uint32_t i = tid; i < np2; i += kTmaThreads) sidx[i] = i < nb ? (uint16_t)i : kEmpty16;
-      __syncthreads();
+      sync_c();
       for (uint32_t kk = 2; kk <= np2; kk <<= 1) {
         for (uint32_t jj = kk >> 1; jj > 0; jj >>= 1) {
           for (uint32_t i = tid; i < np2; i += kTmaThreads) {
@@ -739,7 +749,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constan
               if (gt == ((i & kk) == 0)) { sidx[i] = y; sidx[l] = x; }
             }
           }
-          __syncthreads();
+          sync_c();
         }
       }
     }
@@ -749,26 +759,26 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constan
     for (uint32_t r = r0; r < r1; ++r) {
       const uint32_t jl = r * 32 + lane;
       if (jl < nq) {
-        const K k = pk[jl];
+        const K key = pk[jl];
         uint32_t out = kNoMatch, m = 0;
         if (!has_dup) {
-          uint32_t sl = slot_of(k, cap_log2);
+          uint32_t sl = slot_of(key, cap_log2);
           while (true) {
             const uint32_t e = tab[sl];
             if (e == kNoMatch) break;
-            if (bk[e] == k) { out = e; m = 1; break; }
+            if (bk[e] == key) { out = e; m = 1; break; }
             sl = (sl + 1) & cmask;
           }
         } else {
           uint32_t lo = 0, hi = nb;
           while (lo < hi) {
             const uint32_t mid = (lo + hi) >> 1;
-            if (bk[sidx[mid]] < k) lo = mid + 1; else hi = mid;
+            if (bk[sidx[mid]] < key) lo = mid + 1; else hi = mid;
           }
           uint32_t lo2 = lo, hi2 = nb;
           while (lo2 < hi2) {
             const uint32_t mid = (lo2 + hi2) >> 1;
-            if (bk[sidx[mid]] <= k) lo2 = mid + 1; else hi2 = mid;
+            if (bk[sidx[mid]] <= key) lo2 = mid + 1; else hi2 = mid;
           }
           m = lo2 - lo;
           out = (lo << 16) | m;
@@ -781,7 +791,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constan
     }
     wcount = dev::warp_sum(wcount);
     if (lane == 0) s_wcount[warp] = wcount;
-    __syncthreads();
+    sync_c();  // every probe of this unit is done: the table may be rebuilt after this
+    if (!WRITE) release(b);
     if (warp == 1) {
       const uint64_t wc = lane < kTmaWarps ? s_wcount[lane] : 0;
       const uint64_t inc = dev::warp_inclusive_sum(wc);
@@ -793,27 +804,20 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constan
         base = dev::warp_lookback(a.status, u, tot, a.epoch, a.err);
         if (lane == 0 && u + 1 == units) *a.total_out = base + tot;
       } else {
-        base = __shfl_sync(0xffffffffu, unit_base, 0);
+        base = s_ubase[b];
       }
       if (lane < kTmaWarps) s_wbase[lane] = base + inc - wc;
       if (!WRITE && lane == kTmaWarps - 1) a.unit_counts[u] = inc;
     }
-    if (!WRITE) {
-      // two stages: shared state is rewritten only after the next barrier
-      if (a.stages == 1) {
-        __syncthreads();
-        if (tid == 0) issue_next(0);
-      }
-      continue;
-    }
-    __syncthreads();
+    if (!WRITE) continue;
+    sync_c();
 
     // 3. emit finished rows in probe order at the unit's offset
     const uint32_t bsh4 = (uint32_t)(inf.b_lo & 3), bsh8 = (uint32_t)(inf.b_lo & 1);
     const uint32_t qsh4 = (uint32_t)(inf.q_lo & 3), qsh8 = (uint32_t)(inf.q_lo & 1);
-    auto write_row = [&](uint64_t oo, uint32_t li, uint32_t jl, K k) {
+    auto write_row = [&](uint64_t oo, uint32_t li, uint32_t jl, K key) {
       const uint64_t gi = inf.b_lo + li, j = inf.q_lo + jl;
-      if (a.key_out) static_cast<K*>(a.key_out)[oo] = k;
+      if (a.key_out) static_cast<K*>(a.key_out)[oo] = key;
       if (a.ids_r) a.ids_r[oo] = a.carried_r ? a.carried_r[gi] : (uint32_t)gi;
       if (a.ids_s) a.ids_s[oo] = a.carried_s ? a.carried_s[j] : (uint32_t)j;
       for (int c = 0; c < a.nr; ++c) {
@@ -831,36 +835,26 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_phj_tma(const __grid_constan
     };
     if (!has_dup) {
       emit_compact<K>(a, inf, st, pk, nullptr, res, r0, r1, nq, s_wbase, s_wcount, res + a.qchunk);
-      __syncthreads();
-      if (a.stages == 1 && tid == 0) issue_next(0);
+      release(b);
+      sync_c();
       continue;
     }
     uint64_t o = s_wbase[warp];
     for (uint32_t r = r0; r < r1; ++r) {
       const uint32_t jl = r * 32 + lane;
       const uint32_t e = jl < nq ? res[jl] : kNoMatch;
-      if (!has_dup) {
-        const bool hit = e != kNoMatch;
-        const uint32_t bal = __ballot_sync(0xffffffffu, hit);
-        if (hit) {
-          const uint64_t oo = o + __popc(bal & dev::lanemask_lt());
-          if (oo < a.capacity) write_row(oo, e, jl, bk[e]);
-        }
-        o += __popc(bal);
-      } else {
-        const uint32_t m = e == kNoMatch ? 0 : (e & 0xffffu);
-        const uint32_t lb = e >> 16;
-        const uint32_t inc = dev::warp_inclusive_sum(m);
-        uint64_t oo = o + inc - m;
-        for (uint32_t t = 0; t < m; ++t, ++oo) {
-          const uint32_t li = sidx[lb + t];
-          if (oo < a.capacity) write_row(oo, li, jl, bk[li]);
-        }
-        o += __shfl_sync(0xffffffffu, inc, 31);
+      const uint32_t m = e == kNoMatch ? 0 : (e & 0xffffu);
+      const uint32_t lb = e >> 16;
+      const uint32_t inc = dev::warp_inclusive_sum(m);
+      uint64_t oo = o + inc - m;
+      for (uint32_t t = 0; t < m; ++t, ++oo) {
+        const uint32_t li = sidx[lb + t];
+        if (oo < a.capacity) write_row(oo, li, jl, bk[li]);
       }
+      o += __shfl_sync(0xffffffffu, inc, 31);
     }
-    __syncthreads();
-    if (a.stages == 1 && tid == 0) issue_next(0);
+    release(b);
+    sync_c();
   }
 }
 
@@ -977,7 +971,7 @@ uint64_t run_find(cj_ctx* ctx, FindArgs a, uint64_t total_units) {
       CJ_CUDA(cudaFuncSetAttribute(k_phj_tma<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)tma_smem));
       ctx->kbegin("phj_find", 0);
-      k_phj_tma<K, true><<<grid, kTmaThreads, tma_smem, ctx->stream>>>(a);
+      k_phj_tma<K, true><<<grid, kTmaThreads + 32, tma_smem, ctx->stream>>>(a);
       ctx->kend();
       CJ_CUDA(cudaGetLastError());
       uint64_t* h = reinterpret_cast<uint64_t*>(ctx->host_pinned);
@@ -1004,7 +998,7 @@ uint64_t run_find(cj_ctx* ctx, FindArgs a, uint64_t total_units) {
       CJ_CUDA(cudaFuncSetAttribute(k_phj_tma<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem_c));
       ctx->kbegin("phj_count", (uint64_t)(sizeof(K)) * (a.nb_rows + a.np_rows));
-      k_phj_tma<K, false><<<grid_c, kTmaThreads, smem_c, ctx->stream>>>(ac);
+      k_phj_tma<K, false><<<grid_c, kTmaThreads + 32, smem_c, ctx->stream>>>(ac);
       ctx->kend();
       scan_counts(ctx, counts.as<uint64_t>(), U, offs.as<uint64_t>(), a.total_out);
       CJ_CUDA(cudaGetLastError());
@@ -1018,7 +1012,7 @@ uint64_t run_find(cj_ctx* ctx, FindArgs a, uint64_t total_units) {
         CJ_CUDA(cudaFuncSetAttribute(k_phj_tma<K, true>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tma_smem));
         ctx->kbegin("phj_find", 0);
-        k_phj_tma<K, true><<<grid, kTmaThreads, tma_smem, ctx->stream>>>(a);
+        k_phj_tma<K, true><<<grid, kTmaThreads + 32, tma_smem, ctx->stream>>>(a);
         ctx->kend();
         CJ_CUDA(cudaGetLastError());
       }
