@@ -608,18 +608,37 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
     auto bytes = [&](uint64_t lo, uint64_t hi, uint32_t w) {
       return (uint32_t)((dev::align_hi(hi, w) - dev::align_lo(lo, w)) * w);
     };
+    // what a unit's staging needs from global memory, loaded one unit ahead
+    // so the loads' latency overlaps the previous unit's wait and issue
+    struct Pf {
+      UnitDesc d;
+      uint32_t dup;
+      uint64_t cnt, base;
+    };
+    auto fetch = [&](uint64_t uu) {
+      Pf p;
+      p.d = descs[uu];
+      p.dup = WRITE && a.match_e != nullptr ? a.unit_dup[uu] : 1u;
+      p.cnt = WRITE && a.unit_counts ? a.unit_counts[uu] : ~0ull;
+      p.base = WRITE && a.unit_off ? a.unit_off[uu] : 0ull;
+      return p;
+    };
+    Pf nx{};
+    if (u_begin < u_end) nx = fetch(u_begin);
     uint32_t k = 0;
     for (uint64_t u = u_begin; u < u_end; u += step, ++k) {
+      const Pf cur = nx;
+      if (u + step < u_end) nx = fetch(u + step);
       const int b = (int)(k % (uint32_t)S);
       if (k >= (uint32_t)S) dev::mbar_wait(&empty[b], ((k / S) - 1) & 1u);
-      const UnitDesc d = descs[u];
+      const UnitDesc d = cur.d;
       // pre: the count pass resolved this unit's matches (match_e); no build keys needed
-      const bool pre = WRITE && a.match_e != nullptr && a.unit_dup[u] == 0;
+      const bool pre = WRITE && cur.dup == 0;
       s_desc[b] = d;
       s_pre[b] = pre;
       if (WRITE) {
-        s_ucnt[b] = pre && a.unit_counts ? a.unit_counts[u] : ~0ull;
-        s_ubase[b] = a.unit_off ? a.unit_off[u] : 0;
+        s_ucnt[b] = pre ? cur.cnt : ~0ull;
+        s_ubase[b] = cur.base;
       }
       uint8_t* st = smem + (size_t)b * a.stage_bytes;
       uint32_t total = bytes(d.q_lo, d.q_hi, kb);

@@ -70,6 +70,7 @@ struct SmjArgs {
   uint16_t* match_e;
   uint8_t* tile_pre;
   uint32_t off_e;
+  int nstages;               // TMA stage ring depth (2..kSmjMaxStages)
 };
 
 template <class K>
@@ -348,18 +349,19 @@ __device__ __forceinline__ void smj_emit_rows(const SmjArgs& a, const SmjDesc& d
 // them back per warp (empty barriers), so a warp that finishes a tile early
 // starts the next one instead of waiting for the slowest warp.  Consumer-wide
 // steps of the general path synchronise on named barrier 1 (512 threads).
-constexpr int kSmjStages = 2;
+constexpr int kSmjMaxStages = 4;
 
 template <class K, bool WRITE>
 __global__ void __launch_bounds__(kTmaThreads + 32, 1) k_smj_tma(const __grid_constant__ SmjArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
-  uint32_t* loff = reinterpret_cast<uint32_t*>(smem + kSmjStages * (size_t)a.stage_bytes);
+  const int NS = a.nstages;
+  uint32_t* loff = reinterpret_cast<uint32_t*>(smem + NS * (size_t)a.stage_bytes);
   uint32_t* mcnt = loff + kTileS;
   uint32_t* list = mcnt + kTileS;  // [kSmjList] (WRITE)
-  __shared__ SmjDesc s_desc[kSmjStages];
-  __shared__ bool s_pre[kSmjStages];
-  __shared__ uint64_t s_fcnt[kSmjStages], s_fbase[kSmjStages];
-  __shared__ __align__(8) uint64_t full[kSmjStages], empty[kSmjStages];
+  __shared__ SmjDesc s_desc[kSmjMaxStages];
+  __shared__ bool s_pre[kSmjMaxStages];
+  __shared__ uint64_t s_fcnt[kSmjMaxStages], s_fbase[kSmjMaxStages];
+  __shared__ __align__(8) uint64_t full[kSmjMaxStages], empty[kSmjMaxStages];
   __shared__ uint64_t s_wcnt[2][kTmaWarps], s_wb[2][kTmaWarps];  // by tile parity
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const SmjDesc* __restrict__ descs = static_cast<const SmjDesc*>(a.desc);
@@ -370,7 +372,7 @@ __global__ void __launch_bounds__(kTmaThreads + 32, 1) k_smj_tma(const __grid_co
     return hi > lo ? (uint32_t)((dev::align_hi(hi, w) - dev::align_lo(lo, w)) * w) : 0u;
   };
   if (tid == 0) {
-    for (int i = 0; i < kSmjStages; ++i) {
+    for (int i = 0; i < NS; ++i) {
       dev::mbar_init(&full[i], 1);
       dev::mbar_init(&empty[i], kTmaWarps);
     }
@@ -380,18 +382,36 @@ __global__ void __launch_bounds__(kTmaThreads + 32, 1) k_smj_tma(const __grid_co
 
   if (warp == kTmaWarps) {  // ---- producer ----
     if (lane != 0) return;
+    // what a tile's staging needs from global memory, loaded one tile ahead
+    // so the loads' latency overlaps the previous tile's wait and issue
+    struct Pf {
+      SmjDesc d;
+      uint32_t pre;
+      uint64_t cnt, base;
+    };
+    auto fetch = [&](uint64_t tt) {
+      Pf p;
+      p.d = descs[tt];
+      p.pre = WRITE && a.match_e != nullptr ? a.tile_pre[tt] : 0u;
+      p.cnt = WRITE && a.tile_counts != nullptr ? a.tile_counts[tt] : ~0ull;
+      p.base = WRITE && a.tile_counts != nullptr ? a.tile_off[tt] : 0ull;
+      return p;
+    };
+    Pf nx{};
+    if (blockIdx.x < a.tiles) nx = fetch(blockIdx.x);
     uint32_t k = 0;
     for (uint64_t t = blockIdx.x; t < a.tiles; t += g, ++k) {
-      const int b = (int)(k % kSmjStages);
-      if (k >= kSmjStages) dev::mbar_wait(&empty[b], ((k / kSmjStages) - 1) & 1u);
-      const SmjDesc d = descs[t];
-      const bool pre = WRITE && a.match_e != nullptr && a.tile_pre[t] != 0;
+      const Pf cur = nx;
+      if (t + g < a.tiles) nx = fetch(t + g);
+      const int b = (int)(k % (uint32_t)NS);
+      if (k >= (uint32_t)NS) dev::mbar_wait(&empty[b], ((k / (uint32_t)NS) - 1) & 1u);
+      const SmjDesc d = cur.d;
+      const bool pre = cur.pre != 0;
       s_desc[b] = d;
       s_pre[b] = pre;
       if (WRITE) {
-        const bool f = pre && a.tile_counts != nullptr;
-        s_fcnt[b] = f ? a.tile_counts[t] : ~0ull;
-        s_fbase[b] = f ? a.tile_off[t] : 0;
+        s_fcnt[b] = pre ? cur.cnt : ~0ull;
+        s_fbase[b] = cur.base;
       }
       uint8_t* st = smem + (size_t)b * a.stage_bytes;
       const bool win = d.r_hi - d.r_lo <= a.wmax;
@@ -430,11 +450,11 @@ __global__ void __launch_bounds__(kTmaThreads + 32, 1) k_smj_tma(const __grid_co
   };
   uint32_t k = 0;
   for (uint64_t t = blockIdx.x; t < a.tiles; t += g, ++k) {
-    const int b = (int)(k % kSmjStages);
+    const int b = (int)(k % (uint32_t)NS);
     const int par = (int)(k & 1u);
     uint64_t* s_wcount = s_wcnt[par];
     uint64_t* s_wbase = s_wb[par];
-    dev::mbar_wait(&full[b], (k / kSmjStages) & 1u);
+    dev::mbar_wait(&full[b], (k / (uint32_t)NS) & 1u);
     const SmjDesc d = s_desc[b];
     const bool pre = s_pre[b];
     uint64_t tile_base = 0;
@@ -651,18 +671,26 @@ size_t smj_layout_w(SmjArgs& a, bool write, uint32_t wmax) {
   }
   a.stage_bytes = (uint32_t)off;
   // loff + mcnt [kTileS] each, list [kSmjList] (fill)
-  return 2 * off + 2 * sizeof(uint32_t) * kTileS + (write ? sizeof(uint32_t) * kSmjList : 0);
+  return (size_t)a.nstages * off + 2 * sizeof(uint32_t) * kTileS +
+         (write ? sizeof(uint32_t) * kSmjList : 0);
 }
 
 // Largest r window (shared-memory keys + R payloads) whose two stages fit.
 template <class K>
 size_t smj_layout(SmjArgs& a, bool write) {
+  // fill: three stages (two tiles in flight behind the one being emitted);
+  // count: two (two CTAs per SM); fewer when the rows are too wide
+  const char* e = std::getenv("CJ_SMJ_STAGES");
+  const int want = e ? std::max(2, std::min(kSmjMaxStages, std::atoi(e))) : (write ? 3 : 2);
   size_t smem = 0;
-  for (uint32_t w : {4096u, 2048u, 1024u, 512u}) {
-    smem = smj_layout_w<K>(a, write, w);
-    if (smem <= 200 * 1024) break;
+  for (a.nstages = want; a.nstages >= 2; --a.nstages) {
+    for (uint32_t w : {4096u, 2048u, 1024u, 512u}) {
+      smem = smj_layout_w<K>(a, write, w);
+      if (smem <= 200 * 1024) return smem;
+    }
   }
-  return smem;
+  a.nstages = 2;
+  return smj_layout_w<K>(a, write, 512);
 }
 
 template <class K>
