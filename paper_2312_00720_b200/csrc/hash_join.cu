@@ -564,13 +564,10 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
   const uint32_t kb = sizeof(K);
   const int S = a.stages;
 
-  // Unit order: with precomputed unit offsets (two passes) each CTA walks a
-  // contiguous range of units, so the probe chunks of one build chunk (a large
-  // or skewed probe partition) follow each other and reuse the build table;
-  // the single-pass look-back mode needs units in flight in global order
-  // (round robin).
-  const bool lookback = WRITE && a.unit_off == nullptr;
-  const bool blocked = !lookback && a.np_rows > 0 && a.blocked;
+  // Unit order: round robin over the CTAs, or (a.blocked) a contiguous range
+  // of units per CTA, so the probe chunks of one build chunk (a large or
+  // skewed probe partition) follow each other and reuse the build table.
+  const bool blocked = a.np_rows > 0 && a.blocked;
   // blocked ranges split the probe rows evenly (unit q_lo is monotone): units
   // differ in size (a skewed partition's full chunks vs small ones)
   auto first_unit = [&](uint64_t c) -> uint64_t {  // first unit with q_lo >= c * |S| / grid
@@ -815,17 +812,7 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
     if (warp == 1) {
       const uint64_t wc = lane < kTmaWarps ? s_wcount[lane] : 0;
       const uint64_t inc = dev::warp_inclusive_sum(wc);
-      uint64_t base;
-      if (lookback) {
-        // single pass: the unit's output offset by decoupled look-back over
-        // the units in order (every CTA is resident; units are taken in order)
-        const uint64_t tot = __shfl_sync(0xffffffffu, inc, kTmaWarps - 1);
-        base = dev::warp_lookback(a.status, u, tot, a.epoch, a.err);
-        if (lane == 0 && u + 1 == units) *a.total_out = base + tot;
-      } else {
-        base = s_ubase[b];
-      }
-      if (lane < kTmaWarps) s_wbase[lane] = base + inc - wc;
+      if (lane < kTmaWarps) s_wbase[lane] = s_ubase[b] + inc - wc;
       if (!WRITE && lane == kTmaWarps - 1) a.unit_counts[u] = inc;
     }
     if (!WRITE) continue;
@@ -979,27 +966,6 @@ uint64_t run_find(cj_ctx* ctx, FindArgs a, uint64_t total_units) {
     // count pass (keys only) -> scan -> fill pass; no inter-CTA waiting
     const uint64_t U = total_units;
     uint64_t total = 0;
-    const char* fm = std::getenv("CJ_FIND_PASSES");
-    if (U > 0 && a.write && fm && std::strcmp(fm, "1") == 0) {
-      // one pass: unit offsets by look-back inside the fill kernel
-      const unsigned grid =
-          (unsigned)std::min<uint64_t>((uint64_t)ctx->num_sms * find_ctas_per_sm(), U);
-      a.unit_off = nullptr;
-      a.match_e = nullptr;
-      a.unit_dup = nullptr;
-      CJ_CUDA(cudaFuncSetAttribute(k_phj_tma<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)tma_smem));
-      ctx->kbegin("phj_find", 0);
-      k_phj_tma<K, true><<<grid, kTmaThreads + 32, tma_smem, ctx->stream>>>(a);
-      ctx->kend();
-      CJ_CUDA(cudaGetLastError());
-      uint64_t* h = reinterpret_cast<uint64_t*>(ctx->host_pinned);
-      CJ_CUDA(cudaMemcpyAsync(h, a.total_out, 8, cudaMemcpyDeviceToHost, ctx->stream));
-      CJ_CUDA(cudaStreamSynchronize(ctx->stream));
-      total = h[0];
-      if (total > a.capacity) atomicOr_host_overflow(ctx);
-      return total;
-    }
     if (U > 0) {
       Scratch counts(ctx, U * 8), offs(ctx, U * 8);
       FindArgs ac = a;
