@@ -160,6 +160,7 @@ struct FindArgs {
   uint8_t* unit_dup;
   uint32_t off_e;            // stage offset of the match_e chunk
   int blocked;               // CTAs walk contiguous unit ranges (else round robin)
+  uint32_t group;            // round robin over groups of this many consecutive units
 };
 
 template <class K>
@@ -583,7 +584,8 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
   uint64_t u_begin = 0, u_end = units;
   if (tid == 0) {
     u_end = blocked ? (blockIdx.x + 1 == gridDim.x ? units : first_unit(blockIdx.x + 1)) : units;
-    u_begin = blocked ? (blockIdx.x == 0 ? 0 : first_unit(blockIdx.x)) : blockIdx.x;
+    u_begin = blocked ? (blockIdx.x == 0 ? 0 : first_unit(blockIdx.x))
+                      : (uint64_t)blockIdx.x * a.group;
   }
   __shared__ uint64_t s_range[2];
   if (tid == 0) {
@@ -598,7 +600,15 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
   __syncthreads();
   u_begin = s_range[0];
   u_end = s_range[1];
-  const uint64_t step = blocked ? 1 : gridDim.x;
+  // round robin over groups of a.group consecutive units: the probe chunks of
+  // one build chunk (C3's wide rows: ~4 per partition) mostly land in one CTA
+  // and reuse its table, while a skewed partition's many units still spread
+  // over every CTA
+  const uint64_t G = a.group;
+  auto next_u = [&](uint64_t uu) -> uint64_t {
+    if (blocked || (uu + 1) % G != 0) return uu + 1;
+    return (uu / G + gridDim.x) * G;
+  };
 
   if (producer) {  // ---- producer (one thread) ----
     if (lane != 0) return;
@@ -623,9 +633,9 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
     Pf nx{};
     if (u_begin < u_end) nx = fetch(u_begin);
     uint32_t k = 0;
-    for (uint64_t u = u_begin; u < u_end; u += step, ++k) {
+    for (uint64_t u = u_begin; u < u_end; u = next_u(u), ++k) {
       const Pf cur = nx;
-      if (u + step < u_end) nx = fetch(u + step);
+      if (next_u(u) < u_end) nx = fetch(next_u(u));
       const int b = (int)(k % (uint32_t)S);
       if (k >= (uint32_t)S) dev::mbar_wait(&empty[b], ((k / S) - 1) & 1u);
       const UnitDesc d = cur.d;
@@ -670,7 +680,7 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
   };
   uint64_t built_lo = ~0ull, built_hi = 0;  // build chunk whose table is in shared memory
   uint32_t k = 0;
-  for (uint64_t u = u_begin; u < u_end; u += step, ++k) {
+  for (uint64_t u = u_begin; u < u_end; u = next_u(u), ++k) {
     const int b = (int)(k % (uint32_t)S);
     uint64_t* s_wcount = s_wcnt[k & 1u];
     uint64_t* s_wbase = s_wb[k & 1u];
@@ -1071,6 +1081,8 @@ FindArgs base_args(const void* bkeys, const uint64_t* boff, const void* pkeys,
   a.stages = find_stages();
   const char* order = std::getenv("CJ_FIND_ORDER");
   a.blocked = order && std::strcmp(order, "blocked") == 0;
+  const char* grp = std::getenv("CJ_FIND_GROUP");
+  a.group = grp ? (uint32_t)std::max(1, std::atoi(grp)) : 4;
   return a;
 }
 
