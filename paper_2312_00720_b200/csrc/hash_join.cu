@@ -7,17 +7,21 @@
 //   hash_match_count     hash_match.cpp:212-248
 //   hash_match_fill      hash_match.cpp:250-302  (order: unit, probe pos, build pos)
 //
-// Design (B200): work units are (partition, build chunk, probe chunk of <= 4096
-// rows); splitting the probe side keeps a Zipf hot partition spread over many
-// CTAs while the concatenation in unit order is exactly the reference's
-// emission order.  A persistent CTA takes unit tickets in order, stages the
-// build chunk's keys (and, fused, its transformed payload columns) in shared
-// memory, builds a 16-bit open-addressing table of chunk positions with CAS
-// (duplicate keys are detected exactly during insertion), probes, publishes
-// the unit's match count and resolves its output offset by warp-cooperative
-// decoupled look-back, then writes its rows in probe order.  Chunks holding
-// duplicate keys switch to a stably sorted chunk (bitonic over (key, pos)) so
-// every probe emits its matches in build insertion order.
+// Design (B200): work units are (partition, build chunk, probe chunk);
+// splitting the probe side keeps a Zipf hot partition spread over many CTAs
+// while the concatenation in unit order is exactly the reference's emission
+// order.  Two implementations:
+//  - run_join's path (inputs padded for bulk copies): k_phj_tma, a count pass
+//    -> scan of the unit counts -> fill pass.  Each persistent CTA has a
+//    producer warp that stages units (descriptor, bulk copies) and 16
+//    consumer warps; the count pass builds a 16-bit open-addressing table of
+//    chunk positions with CAS (duplicate keys detected exactly during
+//    insertion), probes, and hands every probe row's match index to the fill,
+//    which then needs neither the table nor the build keys;
+//  - the operator API on arbitrary buffers: k_phj_find, one pass whose units
+//    chain their output offsets by warp-cooperative decoupled look-back.
+// Chunks holding duplicate keys switch to a stably sorted chunk (bitonic over
+// (key, pos)) so every probe emits its matches in build insertion order.
 #include <cuda_runtime.h>
 
 #include <algorithm>
