@@ -8,15 +8,17 @@
 // Output: every (i, j) with r[i] == s[j] in (s-position, r-position) order,
 // output key = s[j]; pk_fk emits only the lower bound (merge_match.cpp:65-68).
 //
-// Design (B200): persistent CTAs take tiles of 2048 consecutive probe (s)
-// positions in ticket order.  A tile's r window [lower_bound(s[j0]),
-// upper_bound(s[j1-1])) is found by two global binary searches and staged in
-// shared memory (merge path: equal work per tile on the s side, the window
-// bounded by the keys the tile can match); every probe then finds its r run by
-// a shared-memory binary search.  Per-tile match counts are chained by
-// warp-cooperative decoupled look-back, so rows land at their reference
-// positions in one pass.  Windows larger than shared memory fall back to
-// global binary search (correct, slower; only for sparse probes).
+// Design (B200): tiles of 2048 consecutive probe (s) positions.  A tile's r
+// window [lower_bound(s[j0]), upper_bound(s[j1-1])) bounds the keys it can
+// match (merge path: equal work per tile on the s side).  run_join's path is
+// k_smj_tma: a count pass (window staged in shared memory, every probe's
+// lower bound by interpolation + galloping, PK-FK window indices handed to
+// the fill) -> scan of the tile counts -> fill pass; both warp-specialised
+// (a producer warp stages tiles, 16 consumer warps release them per warp).
+// The operator API on arbitrary buffers uses k_smj_find, one pass whose
+// tiles chain their output offsets by warp-cooperative decoupled look-back.
+// Windows larger than shared memory fall back to global binary searches
+// (correct, slower; only for sparse probes).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -223,13 +225,13 @@ __global__ void __launch_bounds__(kThreads) k_smj_find(const __grid_constant__ S
 
 // ---- TMA-pipelined count / fill (the default for run_join) ------------------
 //
-// Tiles of 2048 probe rows; a bounds kernel finds every tile's r window
-// [lower_bound(s[j0]), upper_bound(s[j1-1])) with one binary search per tile
-// (all tiles in parallel).  Count and fill passes are persistent (one CTA of
-// 512 threads per SM, tile t_k = blockIdx + k * gridDim), bulk-copy the window
-// (keys + transformed R payloads) and the probe tile (keys + transformed S
-// payloads) into one of two shared-memory stages while the previous tile is
-// merged, and chain nothing across CTAs: counts -> scan -> fill.
+// Tiles of 2048 probe rows; a bounds kernel finds every tile's r window with
+// one binary search per tile (all tiles in parallel).  Count and fill passes
+// are persistent (one or two CTAs per SM, tile t_k = blockIdx + k * gridDim)
+// and bulk-copy the window (keys + transformed R payloads) and the probe tile
+// (keys + transformed S payloads) into a ring of shared-memory stages while
+// earlier tiles are merged; nothing is chained across CTAs: counts -> scan ->
+// fill.
 constexpr int kTmaThreads = 512;
 constexpr int kTmaWarps = kTmaThreads / 32;
 
