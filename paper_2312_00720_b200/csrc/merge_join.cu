@@ -599,9 +599,10 @@ __global__ void __launch_bounds__(kTmaThreads + 32, 1) k_smj_tma(const __grid_co
       consumers_sync();  // loff / mcnt / list are rewritten by the next tile
       continue;
     }
-    // general: per probe, its whole r run (probe rows in rounds of 32)
-    const uint32_t rounds = (nq + 31) / 32;
-    const uint32_t r0 = rounds * warp / kTmaWarps, r1 = rounds * (warp + 1) / kTmaWarps;
+    // general: per probe, its whole r run, in rounds of 32 probe rows over the
+    // same probes whose matches s_wbase[warp] counted (the warp's 32 * kSmjPer
+    // rows; a partial last tile must not redistribute them)
+    const uint32_t r0 = (uint32_t)warp * kSmjPer, r1 = r0 + kSmjPer;
     uint64_t o = s_wbase[warp];
     for (uint32_t rr = r0; rr < r1; ++rr) {
       const uint32_t jl = rr * 32 + lane;

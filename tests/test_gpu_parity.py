@@ -284,3 +284,47 @@ def test_device_generator_matches_reference(ctx, cell):
         assert dg(p, ws[i]) == d[f"r_p{i}"]
     for i, p in enumerate(S.payloads):
         assert dg(p, ws[i]) == d[f"s_p{i}"]
+
+
+def _skewed_keys(kind, n, kb, seed):
+    """Key sets that defeat interpolation in the SMJ count pass's lower-bound
+    guess: geometric gaps, values at both ends of the key range, long runs."""
+    g = np.random.default_rng(seed)
+    top = (1 << (8 * kb)) - 1
+    if kind == "geometric":
+        k = np.unique(np.minimum(np.exp(g.uniform(0, 8 * kb * np.log(2) - 1e-9, n)), top)
+                      .astype(np.uint64))
+    elif kind == "ends":
+        lo = g.integers(0, 64, n // 2, dtype=np.uint64)
+        hi = np.uint64(top) - g.integers(0, 64, n - n // 2, dtype=np.uint64)
+        k = np.concatenate([lo, hi])
+    else:  # runs: few distinct keys, long duplicate runs
+        k = g.integers(0, 7, n, dtype=np.uint64) * np.uint64(top // 8)
+    return k.astype(np.uint32 if kb == 4 else np.uint64)
+
+
+@pytest.mark.parametrize("kb", [4, 8])
+@pytest.mark.parametrize("kind", ["geometric", "ends", "runs"])
+def test_smj_windows_with_skewed_key_gaps(ctx, kb, kind):
+    """The count pass guesses each thread's first lower bound by interpolating
+    between the window's end keys, then steps back and gallops; every key
+    distribution must still give the reference's output exactly."""
+    g = np.random.default_rng(7)
+    rk = _skewed_keys(kind, 3000, kb, 1)
+    uniq = kind != "runs"
+    if uniq:
+        rk = np.unique(rk)
+        g.shuffle(rk)
+    sk = np.concatenate([rk[g.integers(0, rk.size, 9000)], _skewed_keys(kind, 3000, kb, 2)])
+    g.shuffle(sk)
+    R = {"key": rk, "payloads": [g.integers(0, 2 ** 32, rk.size, dtype=np.uint64).astype(np.uint32)]}
+    S = {"key": sk, "payloads": [g.integers(0, 2 ** 32, sk.size, dtype=np.uint64).astype(np.uint32)]}
+    Rd = cj.Relation(cj.to_device(R["key"]), [cj.to_device(p) for p in R["payloads"]], "R", uniq)
+    Sd = cj.Relation(cj.to_device(S["key"]), [cj.to_device(p) for p in S["payloads"]], "S", False)
+    for pattern in ("gftr", "gfur"):
+        out = cj.run_join(ctx, Rd, Sd, "smj", pattern)
+        ref = O.run_join(R, S, "smj", pattern, r_key_unique=uniq)
+        assert out.matches == ref["key"].size
+        assert np.array_equal(H(out.relation.key), ref["key"])
+        for a, b in zip(out.relation.payloads, ref["payloads"]):
+            assert np.array_equal(H(a), b)
