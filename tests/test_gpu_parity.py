@@ -328,3 +328,33 @@ def test_smj_windows_with_skewed_key_gaps(ctx, kb, kind):
         assert np.array_equal(H(out.relation.key), ref["key"])
         for a, b in zip(out.relation.payloads, ref["payloads"]):
             assert np.array_equal(H(a), b)
+
+
+@pytest.mark.parametrize("kb", [4, 8])
+@pytest.mark.parametrize("limit,bits", [(4096, -1), (512, 4), (97, 2)])
+def test_phj_duplicate_builds_split_into_chunks(ctx, kb, limit, bits):
+    """Duplicate-heavy builds whose partitions exceed the sub-partition limit
+    (several build chunks per partition, duplicate-key tables, ragged last
+    probe chunks) against the reference's emission order (C restatement)."""
+    g = np.random.default_rng(11 + kb + limit)
+    rk = (g.zipf(1.3, 5003) % 40).astype(np.uint64) * np.uint64(0x9E3779B1)
+    sk = np.concatenate([rk[g.integers(0, rk.size, 7001)], g.integers(0, 2 ** 20, 999, dtype=np.uint64)])
+    if kb == 4:
+        rk, sk = rk.astype(np.uint32), sk.astype(np.uint32)
+    g.shuffle(sk)
+    R = {"key": rk, "payloads": [g.integers(0, 2 ** 32, rk.size, dtype=np.uint64).astype(np.uint32)]}
+    S = {"key": sk, "payloads": [g.integers(0, 2 ** 63, sk.size, dtype=np.uint64)]}
+    Rd = cj.Relation(cj.to_device(R["key"]), [cj.to_device(p) for p in R["payloads"]], "R", False)
+    Sd = cj.Relation(cj.to_device(S["key"]), [cj.to_device(p) for p in S["payloads"]], "S", False)
+    for pattern in ("gftr", "gfur"):
+        out = cj.run_join(ctx, Rd, Sd, "phj", pattern, sub_partition_limit=limit,
+                          total_radix_bits=bits)
+        ref = O.run_join(R, S, "phj", pattern, total_bits=bits, limit=limit, r_key_unique=False)
+        assert out.matches == ref["key"].size
+        assert np.array_equal(H(out.relation.key), ref["key"])
+        for a, b in zip(out.relation.payloads, ref["payloads"]):
+            assert np.array_equal(H(a), b)
+        # the non-partitioned hash join: same row multiset (its own order)
+        nh = cj.run_join(ctx, Rd, Sd, "nphj", pattern)
+        assert O.canonical_digest([H(nh.relation.key)] + [H(p) for p in nh.relation.payloads]) == \
+            O.canonical_digest([ref["key"]] + ref["payloads"])
