@@ -226,7 +226,9 @@ typedef struct {                   /* SequenceStep (sequence.hpp:10-15) */
   uint64_t rows;                   /* output cardinality of this join */
   uint32_t output_columns;         /* key + carried payloads + dim payload */
   uint64_t transform_ns, find_ns, materialize_ns;
-  uint64_t fk_fetch_ns;            /* gathering the next FK column, between joins */
+  uint64_t fk_fetch_ns;            /* gathering the next FK column, between joins (GFUR;
+                                      GFTR carries the FK columns through the earlier
+                                      joins as probe payloads: 0) */
 } cj_sequence_step;
 
 /* run_join_sequence(fact, dims, algorithm, pattern, options) — sequence.cpp:9-67,

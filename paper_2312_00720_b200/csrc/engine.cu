@@ -1033,7 +1033,12 @@ int cj_run_join_sequence(cj_ctx* ctx, const cj_relation* fact, const cj_relation
           if (p) c->release(p);
       }
     } guard{ctx, &owned};
-    // probe for join 1: (FK_1, ID)  (sequence.cpp:23-27)
+    // probe for join 1: (FK_1, ID)  (sequence.cpp:23-27).  GFTR: the later FK
+    // columns ride along as trailing probe payloads (nfk of them), so each
+    // join's output already holds the next join's FK column in output order —
+    // the reference's FK fetch gather (sequence.cpp:43-55) yields the same
+    // values, and a carried column costs the transform's sequential bytes
+    // instead of a random gather over the fact table.
     cj_relation probe{};
     probe.key = fact->pay[0];
     probe.key_bytes = fact->pay_bytes[0];
@@ -1042,6 +1047,13 @@ int cj_run_join_sequence(cj_ctx* ctx, const cj_relation* fact, const cj_relation
     probe.pay[0] = fact->key;
     probe.pay_bytes[0] = 4;
     probe.key_unique = 0;
+    const bool carry = opt->pattern == CJ_GFTR && n_dims > 1 && n_dims <= CJ_MAX_COLS;
+    uint32_t nfk = 0;
+    if (carry)
+      for (uint32_t d = 1; d < n_dims; ++d, ++nfk) {
+        probe.pay[probe.npay] = fact->pay[d];
+        probe.pay_bytes[probe.npay++] = fact->pay_bytes[d];
+      }
     cudaEvent_t e0, e1;
     CJ_CUDA(cudaEventCreate(&e0));
     CJ_CUDA(cudaEventCreate(&e1));
@@ -1050,7 +1062,7 @@ int cj_run_join_sequence(cj_ctx* ctx, const cj_relation* fact, const cj_relation
       cj::run_join_dev(ctx, &dims[i], &probe, opt, &res);
       cj_sequence_step& st = steps[i];
       st.rows = res.rows;
-      st.output_columns = 1 + dims[i].npay + probe.npay;
+      st.output_columns = 1 + dims[i].npay + probe.npay - nfk;
       st.transform_ns = res.transform_ns;
       st.find_ns = res.find_ns;
       st.materialize_ns = res.materialize_ns;
@@ -1068,39 +1080,46 @@ int cj_run_join_sequence(cj_ctx* ctx, const cj_relation* fact, const cj_relation
       // output payloads are build-side first: (P_i, ID, P_1..P_{i-1}); the
       // next probe is (FK_{i+1}, ID, P_1..P_i)  (sequence.cpp:38-62)
       const uint32_t dim_pay = dims[i].npay;
-      const uint32_t* ids = static_cast<const uint32_t*>(res.pay[dim_pay]);
-      void* next_fk = ctx->alloc(std::max<uint64_t>(res.rows * fact->pay_bytes[i + 1], 16) + cj::kPad);
-      owned.push_back(next_fk);
-      CJ_CUDA(cudaEventRecord(e0, ctx->stream));
-      const void* in[1] = {fact->pay[i + 1]};
-      void* out[1] = {next_fk};
-      const uint32_t by[1] = {fact->pay_bytes[i + 1]};
-      cj::gather_cols(ctx, in, fact->rows, ids, res.rows, out, by, 1);
-      CJ_CUDA(cudaEventRecord(e1, ctx->stream));
-      CJ_CUDA(cudaEventSynchronize(e1));
-      float ms = 0;
-      CJ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-      st.fk_fetch_ns = static_cast<uint64_t>(ms * 1e6);
-      cj::raise_device_errors(ctx);
+      const uint32_t kept = probe.npay - nfk;  // (ID, P_1..P_{i-1})
+      void* next_fk;
+      if (nfk) {  // carried: output column dim_pay + kept is FK_{i+1}
+        next_fk = res.pay[dim_pay + kept];
+        owned.push_back(next_fk);
+      } else {
+        const uint32_t* ids = static_cast<const uint32_t*>(res.pay[dim_pay]);
+        next_fk = ctx->alloc(std::max<uint64_t>(res.rows * fact->pay_bytes[i + 1], 16) + cj::kPad);
+        owned.push_back(next_fk);
+        CJ_CUDA(cudaEventRecord(e0, ctx->stream));
+        const void* in[1] = {fact->pay[i + 1]};
+        void* out[1] = {next_fk};
+        const uint32_t by[1] = {fact->pay_bytes[i + 1]};
+        cj::gather_cols(ctx, in, fact->rows, ids, res.rows, out, by, 1);
+        CJ_CUDA(cudaEventRecord(e1, ctx->stream));
+        CJ_CUDA(cudaEventSynchronize(e1));
+        float ms = 0;
+        CJ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        st.fk_fetch_ns = static_cast<uint64_t>(ms * 1e6);
+        cj::raise_device_errors(ctx);
+      }
       cj_relation np{};
       np.key = next_fk;
       np.key_bytes = fact->pay_bytes[i + 1];
       np.rows = res.rows;
       np.key_unique = 0;
-      const uint32_t total_pay = dims[i].npay + probe.npay;
-      if (total_pay > CJ_MAX_COLS) cj::fail(CJ_ERR_UNSUPPORTED, "too many carried payload columns");
+      if (dim_pay + probe.npay > CJ_MAX_COLS)
+        cj::fail(CJ_ERR_UNSUPPORTED, "too many carried payload columns");
+      // next probe payloads: (ID, P_1..P_{i-1}), P_i, then the FKs still to come
       uint32_t k = 0;
-      for (uint32_t c = dim_pay; c < total_pay; ++c, ++k) {
+      auto take = [&](uint32_t c, uint32_t bytes) {
         np.pay[k] = res.pay[c];
-        np.pay_bytes[k] = c - dim_pay < probe.npay ? probe.pay_bytes[c - dim_pay] : 4;
+        np.pay_bytes[k++] = bytes;
         owned.push_back(res.pay[c]);
-      }
-      for (uint32_t c = 0; c < dim_pay; ++c, ++k) {
-        np.pay[k] = res.pay[c];
-        np.pay_bytes[k] = dims[i].pay_bytes[c];
-        owned.push_back(res.pay[c]);
-      }
+      };
+      for (uint32_t c = 0; c < kept; ++c) take(dim_pay + c, probe.pay_bytes[c]);
+      for (uint32_t c = 0; c < dim_pay; ++c) take(c, dims[i].pay_bytes[c]);
+      for (uint32_t c = kept + 1; c < probe.npay; ++c) take(dim_pay + c, probe.pay_bytes[c]);
       np.npay = k;
+      if (nfk) --nfk;
       ctx->release(res.key);  // the FK key column of the output is not carried
       if (res.ids_r) ctx->release(res.ids_r);
       if (res.ids_s) ctx->release(res.ids_s);
