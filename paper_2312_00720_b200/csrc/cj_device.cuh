@@ -258,9 +258,12 @@ __global__ void k_scan_fix(uint64_t* __restrict__ out, uint64_t n,
 }
 
 // 16-byte aligned superset of an element range, for bulk copies of w-byte elements
-__device__ __forceinline__ uint64_t align_lo(uint64_t i, uint32_t w) { return i & ~(uint64_t)(16 / w - 1); }
+// (w is a power of two <= 16: 16 / w as a shift, not a division — these run
+// ~15 times per staged unit on the producer thread)
+__device__ __forceinline__ uint64_t elems16(uint32_t w) { return 16u >> (__ffs((int)w) - 1); }
+__device__ __forceinline__ uint64_t align_lo(uint64_t i, uint32_t w) { return i & ~(elems16(w) - 1); }
 __device__ __forceinline__ uint64_t align_hi(uint64_t i, uint32_t w) {
-  return (i + 16 / w - 1) & ~(uint64_t)(16 / w - 1);
+  return (i + elems16(w) - 1) & ~(elems16(w) - 1);
 }
 
 }  // namespace dev
