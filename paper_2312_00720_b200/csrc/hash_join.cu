@@ -637,11 +637,18 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
     Pf nx{};
     if (u_begin < u_end) nx = fetch(u_begin);
     uint32_t k = 0;
+    int pb = 0;
+    uint32_t pr = 0;
     for (uint64_t u = u_begin; u < u_end; u = next_u(u), ++k) {
       const Pf cur = nx;
       if (next_u(u) < u_end) nx = fetch(next_u(u));
-      const int b = (int)(k % (uint32_t)S);
-      if (k >= (uint32_t)S) dev::mbar_wait(&empty[b], ((k / S) - 1) & 1u);
+      // stage b of round r = k / S (kept incrementally: no division per tile)
+      const int b = pb;
+      if (k >= (uint32_t)S) dev::mbar_wait(&empty[b], pr ^ 1u);
+      if (++pb == S) {
+        pb = 0;
+        pr ^= 1u;
+      }
       const UnitDesc d = cur.d;
       // pre: the count pass resolved this unit's matches (match_e); no build keys needed
       const bool pre = WRITE && cur.dup == 0;
@@ -684,11 +691,18 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
   };
   uint64_t built_lo = ~0ull, built_hi = 0;  // build chunk whose table is in shared memory
   uint32_t k = 0;
+  int cb = 0;
+  uint32_t cr = 0;
   for (uint64_t u = u_begin; u < u_end; u = next_u(u), ++k) {
-    const int b = (int)(k % (uint32_t)S);
+    const int b = cb;
+    const uint32_t cphase = cr;
+    if (++cb == S) {
+      cb = 0;
+      cr ^= 1u;
+    }
     uint64_t* s_wcount = s_wcnt[k & 1u];
     uint64_t* s_wbase = s_wb[k & 1u];
-    dev::mbar_wait(&full[b], (k / S) & 1u);
+    dev::mbar_wait(&full[b], cphase);
     const UnitDesc inf = s_desc[b];
     const bool pre = s_pre[b];
     const bool reuse = inf.b_lo == built_lo && inf.b_hi == built_hi;

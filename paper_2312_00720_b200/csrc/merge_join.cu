@@ -402,11 +402,18 @@ __global__ void __launch_bounds__(kTmaThreads + 32, 1) k_smj_tma(const __grid_co
     Pf nx{};
     if (blockIdx.x < a.tiles) nx = fetch(blockIdx.x);
     uint32_t k = 0;
+    int pb = 0;
+    uint32_t pr = 0;
     for (uint64_t t = blockIdx.x; t < a.tiles; t += g, ++k) {
       const Pf cur = nx;
       if (t + g < a.tiles) nx = fetch(t + g);
-      const int b = (int)(k % (uint32_t)NS);
-      if (k >= (uint32_t)NS) dev::mbar_wait(&empty[b], ((k / (uint32_t)NS) - 1) & 1u);
+      // stage b of round r = k / NS (kept incrementally: no division per tile)
+      const int b = pb;
+      if (k >= (uint32_t)NS) dev::mbar_wait(&empty[b], pr ^ 1u);
+      if (++pb == NS) {
+        pb = 0;
+        pr ^= 1u;
+      }
       const SmjDesc d = cur.d;
       const bool pre = cur.pre != 0;
       s_desc[b] = d;
@@ -451,12 +458,19 @@ __global__ void __launch_bounds__(kTmaThreads + 32, 1) k_smj_tma(const __grid_co
     if (lane == 0) dev::mbar_arrive(&empty[b]);
   };
   uint32_t k = 0;
+  int cb = 0;
+  uint32_t cr = 0;
   for (uint64_t t = blockIdx.x; t < a.tiles; t += g, ++k) {
-    const int b = (int)(k % (uint32_t)NS);
+    const int b = cb;
+    const uint32_t cphase = cr;
+    if (++cb == NS) {
+      cb = 0;
+      cr ^= 1u;
+    }
     const int par = (int)(k & 1u);
     uint64_t* s_wcount = s_wcnt[par];
     uint64_t* s_wbase = s_wb[par];
-    dev::mbar_wait(&full[b], (k / (uint32_t)NS) & 1u);
+    dev::mbar_wait(&full[b], cphase);
     const SmjDesc d = s_desc[b];
     const bool pre = s_pre[b];
     uint64_t tile_base = 0;
