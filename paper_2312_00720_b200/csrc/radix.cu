@@ -648,7 +648,7 @@ k_scatter_v2(const __grid_constant__ BlockPassArgs a) {
   uint32_t ph0 = 0, ph1 = 0;
   int b = 0;
   uint32_t* mm = &match_word[RANK == 0 ? warp : 0][0];
-  for (uint64_t t = t_begin; t < t_end; ++t, b = (b + 1) % a.stages) {
+  for (uint64_t t = t_begin; t < t_end; ++t, b = b + 1 == a.stages ? 0 : b + 1) {
     if (a.stages == 2 && tid == 0 && t + 1 < t_end && full_tile(t + 1)) {
       dev::fence_proxy_async();
       issue(b ^ 1, t + 1);
