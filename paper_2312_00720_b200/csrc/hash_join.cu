@@ -167,8 +167,13 @@ struct FindArgs {
   uint32_t group;            // round robin over groups of this many consecutive units
 };
 
+// Multiplicative (Fibonacci) hashing as the reference's ChunkTable
+// (hash_match.cpp:24-26); the slot never affects the output (unique chunks
+// match exactly one entry, duplicate chunks are matched through their sorted
+// positions), so 4-byte keys take the 32-bit product (log2cap <= 15).
 template <class K>
 __device__ __forceinline__ uint32_t slot_of(K k, uint32_t log2cap) {
+  if constexpr (sizeof(K) == 4) return ((uint32_t)k * 0x9E3779B1u) >> (32 - log2cap);
   return (uint32_t)(((uint64_t)k * 0x9E3779B97F4A7C15ull) >> (64 - log2cap));
 }
 
@@ -799,7 +804,8 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
     }
 
     // 2. probe from shared memory; warp w owns a contiguous run of rounds
-    uint64_t wcount = 0;
+    uint32_t wcount = 0;  // <= qchunk per unit
+    uint16_t* const me_out = !WRITE && a.match_e ? a.match_e + inf.q_lo : nullptr;
     for (uint32_t r = r0; r < r1; ++r) {
       const uint32_t jl = r * 32 + lane;
       if (jl < nq) {
@@ -828,12 +834,11 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
           out = (lo << 16) | m;
         }
         if (WRITE) res[jl] = out;
-        else if (a.match_e && !has_dup)
-          a.match_e[inf.q_lo + jl] = (uint16_t)(out == kNoMatch ? kEmpty16 : out);
+        else if (me_out && !has_dup) me_out[jl] = (uint16_t)(out == kNoMatch ? kEmpty16 : out);
         wcount += m;
       }
     }
-    wcount = dev::warp_sum(wcount);
+    wcount = (uint32_t)dev::warp_sum((uint64_t)wcount);
     if (lane == 0) s_wcount[warp] = wcount;
     sync_c();  // every probe of this unit is done: the table may be rebuilt after this
     if (!WRITE) release(b);
