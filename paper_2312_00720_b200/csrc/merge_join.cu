@@ -241,7 +241,8 @@ struct SmjDesc {
 
 template <class K>
 __global__ void k_smj_bounds(const K* __restrict__ r, uint64_t nr, const K* __restrict__ s,
-                             uint64_t ns, uint64_t tiles, SmjDesc* __restrict__ desc) {
+                             uint64_t ns, uint64_t tiles, SmjDesc* __restrict__ desc,
+                             uint64_t wide_lim, uint32_t* __restrict__ wide) {
   for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < tiles;
        t += (uint64_t)gridDim.x * blockDim.x) {
     SmjDesc d;
@@ -250,6 +251,7 @@ __global__ void k_smj_bounds(const K* __restrict__ r, uint64_t nr, const K* __re
     d.r_lo = g_lower_bound<K>(r, 0, nr, s[d.s_lo]);
     d.r_hi = g_upper_bound<K>(r, d.r_lo, nr, s[d.s_hi - 1]);
     desc[t] = d;
+    if (wide && d.r_hi - d.r_lo > wide_lim) atomicAdd(wide, 1u);
   }
 }
 
@@ -694,11 +696,12 @@ size_t smj_layout_w(SmjArgs& a, bool write, uint32_t wmax) {
 
 // Largest r window (shared-memory keys + R payloads) whose two stages fit.
 template <class K>
-size_t smj_layout(SmjArgs& a, bool write) {
-  // fill: three stages (two tiles in flight behind the one being emitted);
-  // count: two (two CTAs per SM); fewer when the rows are too wide
+size_t smj_layout(SmjArgs& a, bool write, int stages = 2) {
+  // fill: `stages` (3 keeps two tiles in flight behind the one being emitted
+  // but caps the staged r window at 2048 keys); count: two (two CTAs per SM);
+  // fewer when the rows are too wide
   const char* e = std::getenv("CJ_SMJ_STAGES");
-  const int want = e ? std::max(2, std::min(kSmjMaxStages, std::atoi(e))) : (write ? 3 : 2);
+  const int want = e ? std::max(2, std::min(kSmjMaxStages, std::atoi(e))) : (write ? stages : 2);
   size_t smem = 0;
   for (a.nstages = want; a.nstages >= 2; --a.nstages) {
     for (uint32_t w : {4096u, 2048u, 1024u, 512u}) {
@@ -727,10 +730,19 @@ uint64_t run_tma(cj_ctx* ctx, SmjArgs a) {
     a.tile_pre = pre.as<uint8_t>();
   }
   ctx->kbegin("smj_bounds", a.tiles * (2 * sizeof(K) + 32));
+  // tiles whose r window needs the 4096-key stages (skewed or sparse probes):
+  // the fill takes three stages only when they are rare
+  uint32_t* wide = ctx->ticket(4);
   k_smj_bounds<K><<<grid_for(a.tiles, 128, 4096), 128, 0, ctx->stream>>>(
       static_cast<const K*>(a.r), a.nr, static_cast<const K*>(a.s), a.ns, a.tiles,
-      desc.as<SmjDesc>());
+      desc.as<SmjDesc>(), 2048, a.write ? wide : nullptr);
   ctx->kend();
+  int fill_stages = 2;
+  if (a.write) {
+    CJ_CUDA(cudaMemcpyAsync(ctx->host_pinned, wide, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CJ_CUDA(cudaStreamSynchronize(ctx->stream));
+    fill_stages = (uint64_t)ctx->host_pinned[0] * 64 <= a.tiles ? 3 : 2;
+  }
   SmjArgs ac = a;
   ac.tile_counts = counts.as<uint64_t>();
   const size_t smem_c = smj_layout<K>(ac, false);
@@ -753,7 +765,7 @@ uint64_t run_tma(cj_ctx* ctx, SmjArgs a) {
     a.tile_off = offs.as<uint64_t>();
     const char* ff = std::getenv("CJ_FIND_FAST");
     a.tile_counts = handoff && !(ff && std::strcmp(ff, "0") == 0) ? counts.as<uint64_t>() : nullptr;
-    const size_t smem = smj_layout<K>(a, true);
+    const size_t smem = smj_layout<K>(a, true, fill_stages);
     if (smem > 220 * 1024) fail(CJ_ERR_UNSUPPORTED, "merge join stage exceeds shared memory");
     CJ_CUDA(cudaFuncSetAttribute(k_smj_tma<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));

@@ -465,12 +465,15 @@ __device__ __forceinline__ uint32_t digit_of(K k, const BlockPassArgs& a) {
 }
 
 // One tile of k_scatter_v2 (phases 1-4).  FULL: tile_n == kTile, no guards.
-template <class K, int ITEMS, int RANK, bool SHARD, bool FULL, int RB>
+// HOT: the pass has one dominant digit `hot` (skewed keys): its lanes take
+// their peer mask from one ballot instead of an atomic OR on a single shared
+// word that a third or more of every warp would hit.
+template <class K, int ITEMS, int RANK, bool SHARD, bool FULL, int RB, bool HOT>
 __device__ __forceinline__ void scatter_tile(const BlockPassArgs& a, const uint8_t* st,
                                              uint16_t* sidx, uint16_t (*whist)[1 << RB],
                                              uint32_t* mm, uint32_t* dstart, uint32_t* run,
                                              uint32_t* goff, uint32_t* wsum, uint32_t tbase,
-                                             uint32_t tile_n) {
+                                             uint32_t tile_n, uint32_t hot) {
   constexpr uint32_t kTile = ITEMS * kTmaThreads;
   constexpr int kR = 1 << RB;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -488,7 +491,15 @@ __device__ __forceinline__ void scatter_tile(const BlockPassArgs& a, const uint8
     const uint32_t li = wseg + i * 32 + lane;
     const bool valid = FULL || li < tile_n;
     const uint32_t d = digit_of<SHARD>(skey[li], a);
-    const uint32_t peers = peers_of<RANK>(d, valid, mm, a.bits);
+    uint32_t peers;
+    if constexpr (HOT) {
+      const bool h = valid && d == hot;
+      const uint32_t hb = __ballot_sync(0xffffffffu, h);
+      peers = peers_of<RANK>(d, valid && !h, mm, a.bits);
+      if (h) peers = hb;
+    } else {
+      peers = peers_of<RANK>(d, valid, mm, a.bits);
+    }
     const uint32_t lt = peers & dev::lanemask_lt();
     uint32_t old = 0;
     if (valid && lt == 0) {
@@ -682,12 +693,25 @@ k_scatter_v2(const __grid_constant__ BlockPassArgs a) {
   }
   if (RANK == 0)
     for (int i = tid; i < kTmaWarps * kR; i += kTmaThreads) (&match_word[0][0])[i] = 0;
+  __shared__ uint64_t s_dmax[kR / 32];
   if (tid < kR) {
     uint64_t c = a.base[tid];
     for (uint64_t b2 = 0; b2 < blk; ++b2) c += a.cnt[b2 * a.cnt_stride + tid];
     run[tid] = (uint32_t)c;
+    // the pass's most frequent digit (totals = differences of the bases)
+    const uint64_t tot = (tid + 1 < kR ? a.base[tid + 1] : a.n) - a.base[tid];
+    uint64_t v = (tot << 16) | (uint64_t)tid;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) s_dmax[warp] = v;
   }
   __syncthreads();
+  uint64_t vmax = 0;
+#pragma unroll
+  for (int w = 0; w < kR / 32; ++w) vmax = max(vmax, s_dmax[w]);
+  // >= 1/8 of the rows: a warp round holds 4+ lanes of that digit on average
+  const uint32_t hot = !SHARD && RANK == 0 && (vmax >> 16) * 8 >= a.n ? (uint32_t)(vmax & 0xffffu)
+                                                                         : 0xffffffffu;
 
   uint32_t ph0 = 0, ph1 = 0;
   int b = 0;
@@ -711,8 +735,12 @@ k_scatter_v2(const __grid_constant__ BlockPassArgs a) {
     if (full_tile(t)) {
       dev::mbar_wait(&mbar[b], b ? ph1 : ph0);
       if (b) ph1 ^= 1; else ph0 ^= 1;
-      scatter_tile<K, ITEMS, RANK, SHARD, true, RB>(a, st, sidx, whist, mm, dstart, run, goff, wsum,
-                                                (uint32_t)tbase, tile_n);
+      if (hot != 0xffffffffu)
+        scatter_tile<K, ITEMS, RANK, SHARD, true, RB, true>(a, st, sidx, whist, mm, dstart, run, goff,
+                                                            wsum, (uint32_t)tbase, tile_n, hot);
+      else
+        scatter_tile<K, ITEMS, RANK, SHARD, true, RB, false>(a, st, sidx, whist, mm, dstart, run, goff,
+                                                             wsum, (uint32_t)tbase, tile_n, hot);
     } else {  // last, partial tile: plain loads
       K* wk = reinterpret_cast<K*>(st);
       for (uint32_t j = tid; j < kTile; j += kTmaThreads) wk[j] = j < tile_n ? kin[tbase + j] : K(0);
@@ -729,8 +757,8 @@ k_scatter_v2(const __grid_constant__ BlockPassArgs a) {
         }
       }
       __syncthreads();
-      scatter_tile<K, ITEMS, RANK, SHARD, false, RB>(a, st, sidx, whist, mm, dstart, run, goff, wsum,
-                                                 (uint32_t)tbase, tile_n);
+      scatter_tile<K, ITEMS, RANK, SHARD, false, RB, false>(a, st, sidx, whist, mm, dstart, run, goff,
+                                                            wsum, (uint32_t)tbase, tile_n, hot);
     }
     __syncthreads();
     if (a.stages == 1 && tid == 0 && t + 1 < t_end && full_tile(t + 1)) {
