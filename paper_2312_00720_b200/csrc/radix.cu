@@ -149,23 +149,36 @@ void launch_hist_np(cj_ctx* ctx, const K* keys, const HistArgs& a, int np, uint3
   }
 }
 
-// Totals and exclusive digit bases per pass from the per-block counts
-// (1 block of R threads; thread d owns digit d).
-__global__ void k_digit_bases(const uint32_t* __restrict__ cnt, uint32_t nblocks, int npasses,
-                              uint32_t radix, uint32_t* __restrict__ totals,
-                              uint64_t* __restrict__ base) {
-  __shared__ uint64_t warp_tot[512 / 32];
-  const int d = threadIdx.x;
+// Totals and exclusive digit bases per pass from the per-block counts.  One
+// block of 1024 threads: thread (d, q) sums the blocks b = q (mod split) of
+// digit d (split = 1024 / radix independent load streams instead of one
+// thread per digit walking every block), then threads q = 0 scan the digits.
+__global__ void __launch_bounds__(1024) k_digit_bases(const uint32_t* __restrict__ cnt,
+                                                      uint32_t nblocks, int npasses,
+                                                      uint32_t radix, uint32_t* __restrict__ totals,
+                                                      uint64_t* __restrict__ base) {
+  __shared__ uint64_t warp_tot[256 / 32];
+  __shared__ uint64_t part[1024];
+  const uint32_t split = blockDim.x / radix;
+  const uint32_t d = threadIdx.x % radix, q = threadIdx.x / radix;
   for (int p = 0; p < npasses; ++p) {
-    uint64_t c = 0;
-    for (uint32_t b = 0; b < nblocks; ++b) c += cnt[((uint64_t)b * npasses + p) * radix + d];
-    totals[p * radix + d] = (uint32_t)c;
-    const uint64_t inc = dev::warp_inclusive_sum(c);
-    if ((d & 31) == 31) warp_tot[d >> 5] = inc;
+    uint64_t cq = 0;
+    for (uint32_t b = q; b < nblocks; b += split) cq += cnt[((uint64_t)b * npasses + p) * radix + d];
+    part[threadIdx.x] = cq;
     __syncthreads();
-    uint64_t off = 0;
-    for (int w = 0; w < (d >> 5); ++w) off += warp_tot[w];
-    base[p * radix + d] = off + inc - c;
+    uint64_t c = 0, inc = 0;
+    if (q == 0) {
+      for (uint32_t i = 0; i < split; ++i) c += part[i * radix + d];
+      totals[p * radix + d] = (uint32_t)c;
+      inc = dev::warp_inclusive_sum(c);
+      if ((d & 31) == 31) warp_tot[d >> 5] = inc;
+    }
+    __syncthreads();
+    if (q == 0) {
+      uint64_t off = 0;
+      for (uint32_t w = 0; w < (d >> 5); ++w) off += warp_tot[w];
+      base[p * radix + d] = off + inc - c;
+    }
     __syncthreads();
   }
 }
@@ -913,7 +926,7 @@ void histogram_passes(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes,
   block_hist(ctx, keys, n, key_bytes, plan, g, cnt_dev, hparts);
   const uint32_t R = 1u << g.rb;
   ctx->kbegin("digit_bases", 12ull * R * np);
-  k_digit_bases<<<1, R, 0, ctx->stream>>>(cnt_dev, g.nblocks, np, R, totals_dev, base_dev);
+  k_digit_bases<<<1, 1024, 0, ctx->stream>>>(cnt_dev, g.nblocks, np, R, totals_dev, base_dev);
   ctx->kend();
   CJ_CUDA(cudaGetLastError());
   if (totals_host) {
