@@ -104,7 +104,7 @@ def parse():
     p.add_argument("--scale-log2", type=int, default=0,
                    help="shrink |R|,|S| by 2^k (debug only; the headline uses 0)")
     p.add_argument("--no-extras", action="store_true", help="skip variants/e2e/cpu legs")
-    p.add_argument("--e2e-steps", type=int, default=16,
+    p.add_argument("--e2e-steps", type=int, default=32,
                    help="end-to-end steps (two lanes; more steps amortise the lanes' ramp)")
     return p.parse_args()
 
@@ -476,13 +476,14 @@ def main():
         dist.destroy_process_group()
 
 
-def e2e_leg(ctx, R, S, opt, steps=6, streams=2):
+def e2e_leg(ctx, R, S, opt, steps=32, streams=2):
     """End to end through the host-buffer C-ABI (cj_run_join_host): every step
     uploads its pinned host input columns, joins, and downloads every output
     column into pinned host memory, all inside the timed region.  Steps run
     on `streams` contexts from as many host threads (the C-ABI allows one
     thread per ctx), so one step's download overlaps the next one's upload —
-    PCIe is full duplex.  value = tuples of all timed steps / wall time."""
+    PCIe is full duplex, and the library serialises same-direction copies of
+    concurrent calls.  value = tuples of all timed steps / wall time."""
     import ctypes as C
     import threading
     import torch
@@ -533,11 +534,10 @@ def e2e_leg(ctx, R, S, opt, steps=6, streams=2):
     for t in warm:
         t.join()
     per = [steps // streams + (1 if i < steps % streams else 0) for i in range(streams)]
-    # stagger the lanes by one upload so a lane's download meets the next
-    # lane's upload instead of both lanes moving data the same way at once
-    stagger = lanes[0].h2d.value / 1e9
-    th = [threading.Thread(target=ln.run, args=(k, i * stagger))
-          for i, (ln, k) in enumerate(zip(lanes, per))]
+    # the library lets one host-buffer join per device upload (and one
+    # download) at a time, so the lanes settle into one lane's download next
+    # to the other's upload by themselves
+    th = [threading.Thread(target=ln.run, args=(k,)) for ln, k in zip(lanes, per)]
     t0 = time.perf_counter()
     for t in th:
         t.start()

@@ -212,6 +212,8 @@ int cj_run_join(cj_ctx* ctx, const cj_relation* build, const cj_relation* probe,
 int cj_result_free(cj_ctx* ctx, cj_join_result* res);
 
 /* Host-buffer run_join: the drop-in for coljoin::run_join(const JoinTask&).
+ * Concurrent calls on one device (one ctx per host thread) take turns per
+ * copy direction, so one call's download overlaps another's upload.
  * Uploads the host columns, runs cj_run_join, downloads the output into
  * host buffers allocated by the callback alloc(bytes, user) (e.g. a
  * std::vector resize, or a pinned arena).  Phase times exclude the copies;

@@ -25,6 +25,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "cj_device.cuh"
@@ -1143,10 +1144,20 @@ int cj_result_free(cj_ctx* ctx, cj_join_result* res) {
   return cj::guarded(ctx, [&] { cj::free_output(ctx, res); });
 }
 
+namespace {
+// Host-buffer joins running concurrently on one device (one ctx per host
+// thread) take turns per copy direction: two uploads at once only halve each
+// other's PCIe bandwidth, while an upload next to a download uses both
+// directions of the link.  One lock per direction and device.
+std::mutex g_h2d_mu[16], g_d2h_mu[16];
+}  // namespace
+
 int cj_run_join_host(cj_ctx* ctx, const cj_relation* build, const cj_relation* probe,
                      const cj_join_options* opt, cj_host_alloc_fn alloc, void* user,
                      cj_join_result* out, uint64_t* h2d_ns, uint64_t* d2h_ns) {
   return cj::guarded(ctx, [&] {
+    std::mutex& h2d_mu = g_h2d_mu[ctx->device & 15];
+    std::mutex& d2h_mu = g_d2h_mu[ctx->device & 15];
     cj::validate_relation(build, "a build relation");
     cj::validate_relation(probe, "a probe relation");
     std::vector<void*> owned;
@@ -1176,10 +1187,14 @@ int cj_run_join_host(cj_ctx* ctx, const cj_relation* build, const cj_relation* p
       }
     };
     cj_relation R, S;
-    tm.mark(0);
-    up(build, &R);
-    up(probe, &S);
-    tm.mark(1);
+    {
+      std::lock_guard<std::mutex> lk(h2d_mu);
+      tm.mark(0);
+      up(build, &R);
+      up(probe, &S);
+      tm.mark(1);
+      CJ_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
     cj_join_result dres;
     std::memset(&dres, 0, sizeof(dres));
     cj::run_join_dev(ctx, &R, &S, opt, &dres);
@@ -1190,6 +1205,7 @@ int cj_run_join_host(cj_ctx* ctx, const cj_relation* build, const cj_relation* p
     } rg{ctx, &dres};
     *out = dres;
     const uint64_t t = dres.rows;
+    std::lock_guard<std::mutex> lk(d2h_mu);
     tm.mark(2);
     auto down = [&](const void* src, uint64_t bytes) -> void* {
       void* h = alloc(std::max<uint64_t>(bytes, 1), user);
