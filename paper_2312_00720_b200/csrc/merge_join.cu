@@ -514,11 +514,23 @@ __global__ void __launch_bounds__(kTmaThreads + 32, 1) k_smj_tma(const __grid_co
     } else if (win) {
       uint32_t lb = 0;
       uint16_t e16[kSmjPer];
+      // a window of consecutive keys (dense surrogate keys): key k sits at
+      // k - rk[0]; no search (sorted + span w - 1 => unique and gap-free)
+      const K rlo = w ? rk[0] : K(0);
+      const bool dense = w > 0 && (uint64_t)(rk[w - 1] - rlo) == w - 1;
 #pragma unroll
       for (uint32_t q = 0; q < kSmjPer; ++q) {
         const uint32_t jl = j0 + q;
         e16[q] = 0xffffu;
-        if (jl < nq) {
+        if (jl < nq && dense) {
+          const K k = sk[jl];
+          const bool hit = k >= rlo && (uint64_t)(k - rlo) < w;
+          lb = k < rlo ? 0u : (hit ? (uint32_t)(k - rlo) : (uint32_t)w);
+          loff[jl] = lb;
+          mcnt[jl] = hit;
+          tsum += hit;
+          e16[q] = hit ? (uint16_t)lb : (uint16_t)0xffffu;
+        } else if (jl < nq) {
           const K k = sk[jl];
           if (q == 0) {
             // interpolate between the window's end keys (exact on dense
