@@ -104,6 +104,9 @@ def parse():
     p.add_argument("--scale-log2", type=int, default=0,
                    help="shrink |R|,|S| by 2^k (debug only; the headline uses 0)")
     p.add_argument("--no-extras", action="store_true", help="skip variants/e2e/cpu legs")
+    p.add_argument("--sharded", action="store_true",
+                   help="run the radix-sharded multi-GPU path even on one rank (exercises the "
+                        "shard partition, the NCCL exchange and the per-rank join)")
     p.add_argument("--e2e-steps", type=int, default=32,
                    help="end-to-end steps (two lanes; more steps amortise the lanes' ramp)")
     return p.parse_args()
@@ -269,7 +272,14 @@ def main():
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
-    if world > 1:
+    sharded = world > 1 or a.sharded
+    out_fd = None
+    if sharded:
+        # rank 0 prints exactly one JSON line: NCCL's banner and anything else a
+        # library writes to stdout goes to stderr; the JSON line to the saved fd
+        sys.stdout.flush()
+        out_fd = os.dup(1)
+        os.dup2(2, 1)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ctx = cj.Context(local)
     algo, pattern = a.variant.split("-")
@@ -279,7 +289,7 @@ def main():
     L = A.lib()
     opt = cj.options(algo, pattern)
     shuffle = {"exchange_ms": 0.0, "bytes": 0}
-    if world == 1:
+    if not sharded:
         # headline config: inputs bit-identical to the reference generator
         if "dims" in cfg:
             fact, dims = cj.gen_star(ctx, ns, cfg["dims"], nr, SEED)
@@ -328,7 +338,7 @@ def main():
     for _ in range(a.warmup):
         rows, _ = step()
     torch.cuda.synchronize()
-    if world > 1:
+    if sharded:
         dist.barrier()
     clocks = Clocks(local)
     l0 = ctx.launches
@@ -344,14 +354,14 @@ def main():
     torch.cuda.synchronize()
     launches = ctx.launches - l0
     ms = ev0.elapsed_time(ev1) / a.steps
-    if world > 1:
+    if sharded:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.barrier()
         ms = float(t.item())
     clk = clocks.stop()
     shuffle_info = None
-    if world > 1:
+    if sharded:
         ex = torch.tensor([shuffle["exchange_ms"] / max(a.steps + a.warmup, 1)], device="cuda")
         dist.all_reduce(ex, op=dist.ReduceOp.MAX)
         per_step_bytes = shuffle["bytes"] / max(a.steps + a.warmup, 1)
@@ -423,7 +433,7 @@ def main():
                    "variant": a.variant.upper(), "r_rows": nr, "s_rows": ns, "out_rows": rows,
                    "l2": "inputs >> 126 MB L2 (no flush needed)" if nr >= 1 << 24
                    else "inputs partly L2-resident (small config)",
-                   "parallelism": f"radix-sharded x{world}" if world > 1 else "single GPU"},
+                   "parallelism": f"radix-sharded x{world}" if sharded else "single GPU"},
         "roofline": roofline,
         "join_roofline": {"b_alg_bytes": balg, "b_min_bytes": b_min(nr, ns, rows, kb, ws),
                           "frac_b_alg": balg / (ms / 1e3) / (peak * 1e9),
@@ -442,7 +452,7 @@ def main():
         out["shuffle"] = shuffle_info
         out["config"]["workload"] = (f"C5-shaped weak scaling: |R|={world}x2^27, |S|={world}x2^28 "
                                      "total, 4-byte key + 2 x 4-byte payloads, cj_gen_shard")
-    if rank == 0 and world == 1 and not a.no_extras and a.config == "C2":
+    if rank == 0 and not sharded and not a.no_extras and a.config == "C2":
         # the other variants (3 timed steps each)
         var = {}
         for v in ("phj-gftr", "smj-gftr", "phj-gfur", "smj-gfur", "nphj-gftr", "nphj-gfur"):
@@ -471,8 +481,12 @@ def main():
         out["e2e"] = e2e_leg(ctx, R, S, opt, steps=a.e2e_steps)
         out["cpu_baseline"] = cpu_baseline(nr, ns, a.variant)
     if rank == 0:
-        print(json.dumps(out))
-    if world > 1:
+        if out_fd is not None:
+            sys.stdout.flush()
+            os.write(out_fd, (json.dumps(out) + "\n").encode())
+        else:
+            print(json.dumps(out))
+    if sharded:
         dist.destroy_process_group()
 
 
