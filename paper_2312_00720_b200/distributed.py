@@ -56,8 +56,10 @@ def host_shard_of(keys: np.ndarray, parts: int) -> np.ndarray:
     return np.array([(int(v) * parts) >> 64 for v in x], dtype=np.int64)
 
 
-def exchange(rel, counts, group=None):
-    """all_to_all shuffle of a shard-grouped relation; returns the received rows."""
+def exchange(rel, counts, group=None, async_op=False):
+    """all_to_all shuffle of a shard-grouped relation; returns the received
+    rows, the received counts and (async_op) the pending column transfers,
+    which the caller waits on before reading the rows."""
     import torch
     import torch.distributed as dist
     dev = rel.key.device
@@ -65,12 +67,15 @@ def exchange(rel, counts, group=None):
     recv = torch.empty_like(send)
     dist.all_to_all_single(recv, send, group=group)
     rc = [int(x) for x in recv.tolist()]
-    out_cols = []
+    out_cols, works = [], []
     for col in [rel.key] + list(rel.payloads):
         out = torch.empty(sum(rc), dtype=col.dtype, device=dev)
-        dist.all_to_all_single(out, col, rc, counts, group=group)
+        w = dist.all_to_all_single(out, col, rc, counts, group=group, async_op=async_op)
+        if async_op:
+            works.append(w)
         out_cols.append(out)
-    return cj.Relation(out_cols[0], out_cols[1:], rel.name, rel.key_unique), rc
+    result = cj.Relation(out_cols[0], out_cols[1:], rel.name, rel.key_unique)
+    return (result, rc, works) if async_op else (result, rc)
 
 
 def distributed_join(ctx, build, probe, algo="phj", pattern="gftr", group=None,
@@ -87,13 +92,17 @@ def distributed_join(ctx, build, probe, algo="phj", pattern="gftr", group=None,
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         ev[0].record()
     t0 = time.perf_counter()
+    # R's columns travel while S is partitioned (the collectives run on the
+    # process group's stream; the partition on the ctx stream)
     Rs, rcount = part(build, world)
+    Rr, _, r_works = exchange(Rs, rcount, group, async_op=True)
     Ss, scount = part(probe, world)
     t1 = time.perf_counter()
     if cuda:
         ev[1].record()
-    Rr, _ = exchange(Rs, rcount, group)
     Sr, _ = exchange(Ss, scount, group)
+    for w in r_works:
+        w.wait()
     t2 = time.perf_counter()
     if cuda:
         ev[2].record()
@@ -102,6 +111,7 @@ def distributed_join(ctx, build, probe, algo="phj", pattern="gftr", group=None,
         timings["partition_s"] = t1 - t0
         timings["exchange_s"] = t2 - t1
         if cuda:
+            # (R's exchange overlaps S's partition: partition_ms includes it)
             timings["partition_ms"] = ev[0].elapsed_time(ev[1])
             timings["exchange_ms"] = ev[1].elapsed_time(ev[2])
         sent = sum(c for d, c in enumerate(rcount) if d != dist.get_rank(group))
