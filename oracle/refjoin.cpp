@@ -4,7 +4,8 @@
 // golden fixtures under tests/golden/.
 //
 //   refjoin join  [workload opts] --algo phj|smj --pattern gftr|gfur
-//                 [--reps N] [--warmup W] [--threads T] [--prealloc] [--digest] [--dump DIR]
+//                 [--reps N] [--warmup W] [--threads T] [--prealloc] [--digest] [--pdigest]
+//                 [--dump DIR]   (--pdigest: canonical digest by a parallel sort)
 //   refjoin prim  --n N --seed S [--dump DIR]
 //   refjoin gen   [workload opts] --dump DIR
 //   refjoin star  --fact N --dims D --dim-rows M --seed S --algo phj|smj --pattern gftr|gfur
@@ -28,6 +29,7 @@
 #include <omp.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -84,6 +86,61 @@ uint64_t digest_col(const Column& c) { return digest_words(widen(c)); }
 uint64_t digest_u32(const std::vector<uint32_t>& v) {
   std::vector<uint64_t> w(v.begin(), v.end());
   return digest_words(w);
+}
+
+// Canonical-row digest of a join output, equal to
+// digest_words(oracle::canonical_rows(rel)) (oracle.cpp:77-88: rows widened to
+// u64, sorted lexicographically) but sorted in parallel: T chunk sorts, then
+// rounds of pairwise merges.  Identical rows are interchangeable, so any
+// correct sort gives the reference's flat vector.  The reference's
+// single-threaded index sort takes tens of minutes at 2^28 rows; this is test
+// infrastructure for the full-size golden digests (tests/golden/make_golden.py
+// --full), not a change to the reference.
+template <size_t W>
+uint64_t parallel_canonical_digest_w(const Relation& rel) {
+  using Row = std::array<uint64_t, W>;
+  const size_t n = rel.rows();
+  std::vector<Row> rows(n), tmp(n);
+  std::vector<const Column*> cols{&rel.key};
+  for (const auto& p : rel.payloads) cols.push_back(&p);
+#pragma omp parallel for schedule(static)
+  for (size_t i = 0; i < n; ++i)
+    for (size_t c = 0; c < W; ++c) rows[i][c] = cols[c]->at(i);
+  const size_t T = static_cast<size_t>(std::max(1, omp_get_max_threads()));
+  size_t parts = 1;
+  while (parts < T) parts <<= 1;
+  std::vector<size_t> b(parts + 1);
+  for (size_t p = 0; p <= parts; ++p) b[p] = n * p / parts;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (size_t p = 0; p < parts; ++p) std::sort(rows.begin() + b[p], rows.begin() + b[p + 1]);
+  for (size_t width = 1; width < parts; width <<= 1) {
+#pragma omp parallel for schedule(dynamic, 1)
+    for (size_t p = 0; p < parts; p += 2 * width) {
+      const size_t lo = b[p], mid = b[std::min(p + width, parts)], hi = b[std::min(p + 2 * width, parts)];
+      std::merge(rows.begin() + lo, rows.begin() + mid, rows.begin() + mid, rows.begin() + hi,
+                 tmp.begin() + lo);
+    }
+    rows.swap(tmp);
+  }
+  uint64_t h = 0x12345678ull, i = 0;
+  for (const Row& r : rows)
+    for (size_t c = 0; c < W; ++c, ++i) h = mix64(h ^ r[c]) + i;
+  return h;
+}
+
+uint64_t parallel_canonical_digest(const Relation& rel) {
+  switch (rel.column_count()) {
+    case 1: return parallel_canonical_digest_w<1>(rel);
+    case 2: return parallel_canonical_digest_w<2>(rel);
+    case 3: return parallel_canonical_digest_w<3>(rel);
+    case 4: return parallel_canonical_digest_w<4>(rel);
+    case 5: return parallel_canonical_digest_w<5>(rel);
+    case 6: return parallel_canonical_digest_w<6>(rel);
+    case 7: return parallel_canonical_digest_w<7>(rel);
+    case 8: return parallel_canonical_digest_w<8>(rel);
+    case 9: return parallel_canonical_digest_w<9>(rel);
+    default: return digest_words(oracle::canonical_rows(rel));
+  }
 }
 
 std::vector<unsigned> parse_widths(const char* s) {
@@ -150,12 +207,27 @@ void dump_rel(const std::string& dir, const std::string& tag, const Relation& r)
     dump_col(dir + "/" + tag + "_p" + std::to_string(c) + ".bin", r.payloads[c]);
 }
 
+int join_one(const Args& a, const Relation& r, const Relation& s, JoinAlgo algo, JoinPattern pattern);
+
+// --all-variants: generate once, then run PHJ/SMJ x GFTR/GFUR (one JSON line each)
 int cmd_join(const Args& a) {
   auto [r, s] = make_workload(a);
+  auto algo = std::strcmp(a.get("--algo", "phj"), "smj") == 0 ? JoinAlgo::SMJ : JoinAlgo::PHJ;
+  auto pattern = std::strcmp(a.get("--pattern", "gftr"), "gfur") == 0 ? JoinPattern::GFUR
+                                                                     : JoinPattern::GFTR;
+  if (!a.has("--all-variants")) return join_one(a, r, s, algo, pattern);
+  for (JoinAlgo al : {JoinAlgo::PHJ, JoinAlgo::SMJ})
+    for (JoinPattern pa : {JoinPattern::GFTR, JoinPattern::GFUR}) {
+      join_one(a, r, s, al, pa);
+      std::fflush(stdout);
+    }
+  return 0;
+}
+
+int join_one(const Args& a, const Relation& r, const Relation& s, JoinAlgo algo, JoinPattern pattern) {
   JoinTask task;
-  task.algorithm = std::strcmp(a.get("--algo", "phj"), "smj") == 0 ? JoinAlgo::SMJ : JoinAlgo::PHJ;
-  task.pattern = std::strcmp(a.get("--pattern", "gftr"), "gfur") == 0 ? JoinPattern::GFUR
-                                                                    : JoinPattern::GFTR;
+  task.algorithm = algo;
+  task.pattern = pattern;
   // --swap: build on S (duplicate keys, key_unique=false), probe with R
   const bool swap = a.has("--swap");
   task.build = swap ? &s : &r;
@@ -179,10 +251,18 @@ int cmd_join(const Args& a) {
   const uint64_t med = totals[totals.size() / 2];
   const double tput = static_cast<double>(r.rows() + s.rows()) / (med * 1e-9);
   std::string dig = "null", odig = "null";
-  if (a.has("--digest")) {
+  if (a.has("--digest") || a.has("--pdigest")) {
     char buf[32];
-    std::snprintf(buf, sizeof(buf), "\"%016llx\"",
-                  (unsigned long long)digest_words(oracle::canonical_rows(out.relation)));
+    // --pdigest: the same digest through the parallel canonical sort
+    // (--digest --pdigest checks that both agree)
+    uint64_t d = 0;
+    if (a.has("--digest")) d = digest_words(oracle::canonical_rows(out.relation));
+    if (a.has("--pdigest")) {
+      const uint64_t pd = parallel_canonical_digest(out.relation);
+      if (a.has("--digest") && pd != d) throw SpecInvalid("parallel canonical digest differs");
+      d = pd;
+    }
+    std::snprintf(buf, sizeof(buf), "\"%016llx\"", (unsigned long long)d);
     dig = buf;
     // emission-order digest over the flat columns (key, then payloads)
     std::vector<uint64_t> flat = widen(out.relation.key);

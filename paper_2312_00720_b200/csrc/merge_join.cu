@@ -514,25 +514,40 @@ __global__ void __launch_bounds__(kTmaThreads + 32, 1) k_smj_tma(const __grid_co
     } else if (win) {
       uint32_t lb = 0;
       uint16_t e16[kSmjPer];
-      // a window of consecutive keys (dense surrogate keys): key k sits at
-      // k - rk[0]; no search (sorted + span w - 1 => unique and gap-free)
+      // a PK-FK window of consecutive keys (dense surrogate keys): key k sits
+      // at k - rk[0]; no search.  Sorted + span w - 1 means gap-free only
+      // when the keys are unique, so the shortcut is PK-FK only (a non-PK
+      // window [5,5,7] has the span of [5,6,7]), and each hit is verified as
+      // the lower bound (rk[i] == k, rk[i-1] < k) so a build mislabelled
+      // unique falls back to the search and keeps merge_match.cpp:65-68's
+      // lower-bound emission.
       const K rlo = w ? rk[0] : K(0);
-      const bool dense = w > 0 && (uint64_t)(rk[w - 1] - rlo) == w - 1;
+      const bool dense = a.pk_fk && w > 0 && (uint64_t)(rk[w - 1] - rlo) == w - 1;
+      bool searched = false;  // lb is a valid galloping start for later probes
 #pragma unroll
       for (uint32_t q = 0; q < kSmjPer; ++q) {
         const uint32_t jl = j0 + q;
         e16[q] = 0xffffu;
+        bool done = false;
         if (jl < nq && dense) {
           const K k = sk[jl];
-          const bool hit = k >= rlo && (uint64_t)(k - rlo) < w;
-          lb = k < rlo ? 0u : (hit ? (uint32_t)(k - rlo) : (uint32_t)w);
-          loff[jl] = lb;
-          mcnt[jl] = hit;
-          tsum += hit;
-          e16[q] = hit ? (uint16_t)lb : (uint16_t)0xffffu;
-        } else if (jl < nq) {
+          const bool inr = k >= rlo && (uint64_t)(k - rlo) < w;
+          const uint32_t i = inr ? (uint32_t)(k - rlo) : 0u;
+          const bool hit = inr && rk[i] == k && (i == 0 || rk[i - 1] < k);
+          if (hit || !inr) {
+            lb = k < rlo ? 0u : (hit ? i : (uint32_t)w);
+            loff[jl] = lb;
+            mcnt[jl] = hit;
+            tsum += hit;
+            e16[q] = hit ? (uint16_t)lb : (uint16_t)0xffffu;
+            searched = true;
+            done = true;
+          }
+        }
+        if (jl < nq && !done) {
           const K k = sk[jl];
-          if (q == 0) {
+          if (!searched) {
+            searched = true;
             // interpolate between the window's end keys (exact on dense
             // keys), then gallop to the lower bound from below
             uint32_t g = 0;

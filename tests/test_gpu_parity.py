@@ -358,3 +358,67 @@ def test_phj_duplicate_builds_split_into_chunks(ctx, kb, limit, bits):
         nh = cj.run_join(ctx, Rd, Sd, "nphj", pattern)
         assert O.canonical_digest([H(nh.relation.key)] + [H(p) for p in nh.relation.payloads]) == \
             O.canonical_digest([ref["key"]] + ref["payloads"])
+
+
+# ---- non-PK SMJ windows whose duplicates stand in for gaps ------------------------
+# merge_match.cpp:53-71: a non-PK walk emits the whole r run of every probe key;
+# a PK-FK walk (pk_fk = build.key_unique, join_engine.cpp:271) emits the lower bound.
+
+def _smj_case(ctx, rk, sk, uniq, seed=0):
+    g = np.random.default_rng(seed)
+    R = {"key": rk, "payloads": [g.integers(0, 2 ** 32, rk.size, dtype=np.uint64).astype(np.uint32)]}
+    S = {"key": sk, "payloads": [g.integers(0, 2 ** 63, sk.size, dtype=np.uint64)]}
+    Rd, Sd = _dev_rel(R, uniq, "R"), _dev_rel(S, False, "S")
+    for algo in ("smj", "phj"):
+        for pattern in ("gftr", "gfur"):
+            out = cj.run_join(ctx, Rd, Sd, algo, pattern)
+            ref = O.run_join(R, S, algo, pattern, r_key_unique=uniq)
+            assert out.matches == ref["key"].size, (algo, pattern)
+            assert np.array_equal(H(out.relation.key), ref["key"]), (algo, pattern)
+            for a, b in zip(out.relation.payloads, ref["payloads"]):
+                assert np.array_equal(H(a), b), (algo, pattern)
+
+
+@pytest.mark.parametrize("uniq", [False, True])
+def test_smj_duplicates_in_place_of_gaps(ctx, uniq):
+    """Build [5,5,7] |x| probe [5,6,7]: the window spans 7-5 = w-1 like a gap-free
+    unique window.  Non-PK: (5,r0,s0),(5,r1,s0),(7,r2,s2).  Mislabelled unique
+    (pk_fk without validation): the lower bound, (5,r0,s0),(7,r2,s2)."""
+    rk = np.array([5, 5, 7], np.uint32)
+    sk = np.array([5, 6, 7], np.uint32)
+    _smj_case(ctx, rk, sk, uniq)
+    R = {"key": rk, "payloads": [np.array([10, 11, 12], np.uint32)]}
+    S = {"key": sk, "payloads": [np.array([20, 21, 22], np.uint32)]}
+    out = cj.run_join(ctx, _dev_rel(R, uniq, "R"), _dev_rel(S, False, "S"), "smj", "gftr")
+    want = ([5, 5, 7], [10, 11, 12], [20, 20, 22]) if not uniq else ([5, 7], [10, 12], [20, 22])
+    assert list(H(out.relation.key)) == want[0]
+    assert list(H(out.relation.payloads[0])) == want[1]
+    assert list(H(out.relation.payloads[1])) == want[2]
+
+
+@pytest.mark.parametrize("logn", [12, 14, 16, 18, 20])
+@pytest.mark.parametrize("kb", [4, 8])
+def test_smj_sparse_duplicate_builds(ctx, logn, kb):
+    """Non-PK builds with about one row per key (uniform draws from [0, n)),
+    probed by every key of [0, n) and some misses, in exact reference order."""
+    n = 1 << logn
+    g = np.random.default_rng(logn * 10 + kb)
+    dt = np.uint32 if kb == 4 else np.uint64
+    rk = g.integers(0, n, n, dtype=np.uint64).astype(dt)
+    sk = np.concatenate([g.permutation(n).astype(np.uint64),
+                         g.integers(n, 2 * n, n // 8, dtype=np.uint64)]).astype(dt)
+    g.shuffle(sk)
+    _smj_case(ctx, rk, sk, False, seed=logn)
+
+
+@pytest.mark.parametrize("kb", [4, 8])
+def test_smj_mislabelled_unique_build(ctx, kb):
+    """A build declared unique that is not (no validation): every variant
+    keeps the reference's PK-FK emission (one match per probe, the lower
+    bound for SMJ, the first inserted for PHJ)."""
+    n = 1 << 15
+    g = np.random.default_rng(99 + kb)
+    dt = np.uint32 if kb == 4 else np.uint64
+    rk = g.integers(0, n, n, dtype=np.uint64).astype(dt)
+    sk = g.permutation(n).astype(dt)
+    _smj_case(ctx, rk, sk, True, seed=kb)
