@@ -107,6 +107,8 @@ def parse():
     p.add_argument("--sharded", action="store_true",
                    help="run the radix-sharded multi-GPU path even on one rank (exercises the "
                         "shard partition, the NCCL exchange and the per-rank join)")
+    p.add_argument("--no-configs", action="store_true",
+                   help="skip the C3/C4 records (PHJ/SMJ-GFTR, 3 timed steps each)")
     p.add_argument("--e2e-steps", type=int, default=32,
                    help="end-to-end steps (two lanes; more steps amortise the lanes' ramp)")
     return p.parse_args()
@@ -178,6 +180,49 @@ class Clocks:
                 "samples": len(rows)}
 
 
+def config_dict(cfg, a, nr, ns, world):
+    """The `config` object of the JSON line; both arms print the same one."""
+    sharded = world > 1 or a.sharded
+    if sharded:
+        wl = (f"C5-shaped weak scaling: |R|={world}x2^27, |S|={world}x2^28 total, 4-byte key + "
+              "2 x 4-byte payloads, cj_gen_shard")
+    else:
+        wl = cfg["desc"] if a.scale_log2 == 0 else f"{a.config}/2^{a.scale_log2}"
+    return {"workload": wl, "variant": a.variant.upper(), "r_rows": nr, "s_rows": ns,
+            "l2": "inputs >> 126 MB L2 (no flush needed)" if nr >= 1 << 24
+            else "inputs partly L2-resident (small config)",
+            "parallelism": f"radix-sharded x{world}" if sharded else "single GPU"}
+
+
+def ref_workload_args(cfg, nr, ns):
+    """refjoin workload flags for a CONFIGS entry (the reference's WorkloadSpec)."""
+    ws = cfg["widths"]
+    args = ["--r", str(nr), "--s", str(ns), "--rpay", str(len(ws)), "--spay", str(len(ws)),
+            "--key", "u64" if cfg["key"] == 8 else "u32", "--pay", "u64" if 8 in ws else "u32",
+            "--match", str(cfg["match"]), "--zipf", str(cfg["zipf"]), "--seed", str(SEED)]
+    if 8 in ws:
+        args += ["--widths", ",".join(str(w) for w in ws)]
+    return args
+
+
+def self_launch(a):
+    """`bench.py --gpus N` outside torchrun: re-exec under torch.distributed.run
+    with N ranks on this node (fails loudly when fewer GPUs are visible)."""
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < a.gpus:
+        sys.exit(f"bench.py: --gpus {a.gpus} but only {have} CUDA device(s) are visible")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={a.gpus}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
 def dist_env():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
             int(os.environ.get("LOCAL_RANK", 0)))
@@ -194,40 +239,49 @@ def reference_arm(a):
                           "unavailable": "oracle/_ref/refjoin not built (needs /root/reference)"}))
         return
     algo, pattern = a.variant.split("-")
-    nr, ns = R_ROWS >> a.scale_log2, S_ROWS >> a.scale_log2
+    if algo == "nphj":
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "the reference has no non-partitioned hash join (SPEC.md)"}))
+        return
+    cfg = CONFIGS[a.config]
+    world = max(world, a.gpus)
+    # the whole job: under N ranks our arm joins N C2-sized shards (weak scaling)
+    nr, ns = (cfg["r"] >> a.scale_log2) * world, (cfg["s"] >> a.scale_log2) * world
     cores = os.cpu_count() or 1
     env = dict(os.environ, OMP_NUM_THREADS=str(cores))
 
     def run(shift, reps, warmup):
-        return O.refjoin("join", "--r", str(nr >> shift), "--s", str(ns >> shift), "--rpay",
-                         str(NPAY), "--spay", str(NPAY), "--seed", str(SEED), "--algo", algo,
+        return O.refjoin("join", *ref_workload_args(cfg, nr >> shift, ns >> shift), "--algo", algo,
                          "--pattern", pattern, "--prealloc", "--threads", str(cores), "--reps",
                          str(reps), "--warmup", str(warmup), env=env)
 
-    # Bounded sample: probe the per-tuple cost at 1/64 of the workload, then pick
-    # the largest same-shape sample (power-of-two shrink of |R| and |S|) whose
-    # K+W run_join calls fit a ~150 s budget.  Smaller samples are more cache
-    # friendly, so the sampled CPU throughput errs in the reference's favour.
+    # The full workload whenever its K+W run_join calls fit the budget (C2 on
+    # 16 cores: ~4.6 s per call, ~2 min for 20+5); otherwise the largest
+    # same-shape power-of-two sample that does, probed at 1/64 first.
+    budget_s = float(os.environ.get("CJ_REF_BUDGET_S", "600"))
     probe = run(6, 1, 0)
     ns_per_tuple = probe["total_ns_mean"] / ((nr >> 6) + (ns >> 6))
     shift = 0
     while shift < 6 and ns_per_tuple * ((nr >> shift) + (ns >> shift)) * (a.steps + a.warmup) \
-            > 150e9:
+            > budget_s * 1e9:
         shift += 1
     r = probe if (shift == 6 and a.steps == 1 and a.warmup == 0) else run(shift, a.steps, a.warmup)
     snr, sns = nr >> shift, ns >> shift
     ms = r["total_ns_mean"] / 1e6
     v = (snr + sns) / (ms / 1e3)
+    sample = (f"|R|={snr}, |S|={sns} ("
+              + ("the whole workload" if shift == 0 else f"1/2^{shift} of the workload, same shape")
+              + f"), mean of {a.steps} timed run_join calls after {a.warmup} warm-up "
+              f"(preallocate=true, {cores} OpenMP threads)")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "tuples/s", "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic (gen_pk_fk, seed 42)",
-        "config": {"workload": WORKLOAD, "variant": a.variant.upper(), "r_rows": nr, "s_rows": ns},
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64" if cfg["key"] == 8 else "u32",
+        "data": "synthetic: the reference's workloads::gen_pk_fk (seed 42), on the host",
+        "config": config_dict(cfg, a, cfg["r"] >> a.scale_log2, cfg["s"] >> a.scale_log2, world),
+        "same_workload": shift == 0,
         "cpu_baseline": {"value": v, "unit": "tuples/s", "cores": cores, "kind": "reference",
-                         "sample": f"|R|=2^{snr.bit_length() - 1}, |S|=2^{sns.bit_length() - 1} "
-                                   f"(1/2^{shift} of the workload, same shape), mean of {a.steps} "
-                                   f"timed run_join calls after {a.warmup} warm-up "
-                                   f"(preallocate=true, {cores} OpenMP threads)"},
+                         "sample": sample},
         "e2e": {"value": v, "unit": "tuples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "phases_ms": {"transform": r["transform_ns"] / 1e6, "find": r["find_ns"] / 1e6,
                       "materialize": r["materialize_ns"] / 1e6},
@@ -262,8 +316,13 @@ def cpu_baseline(nr, ns, variant):
 
 def main():
     a = parse()
+    ws_env = os.environ.get("WORLD_SIZE")
+    if ws_env is not None and int(ws_env) != a.gpus and not (a.gpus == 1 and int(ws_env) > 1):
+        sys.exit(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={ws_env}")
     if a.impl == "reference":
         return reference_arm(a)
+    if a.gpus > 1 and ws_env is None:
+        return self_launch(a)
     import torch
     import torch.distributed as dist
     import paper_2312_00720_b200 as cj
@@ -403,10 +462,17 @@ def main():
                        "alg_gbs": (b / 1e9) / (t / 1e3) if t else None}
                       for n, (c, t, b) in agg.items()), key=lambda d: -d["ms_per_step"])
     dom = kernels[0] if kernels else None
-    traffic = None
+    # DRAM traffic per launch of the dominant kernel: not measurable inside a
+    # timed run (ncu replays kernels), so it comes from the committed ncu
+    # capture of the same kernel, labelled with its source; null when the
+    # capture does not cover this kernel/config
+    traffic, traffic_src = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f).get(dom["kernel"]) if dom else None
+            tj = json.load(f)
+        ent = tj.get(f"{a.config}/{a.variant}/{dom['kernel']}") if dom else None
+        if isinstance(ent, dict):
+            traffic, traffic_src = ent.get("bytes_per_launch"), ent.get("source")
     except Exception:
         pass
     roofline = None
@@ -415,6 +481,7 @@ def main():
         achieved = (b / c) / 1e9 / ((t / c) / 1e3)
         roofline = {"bound": "hbm", "kernel": dom["kernel"], "achieved": achieved, "peak": peak,
                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                    "traffic_source": traffic_src,
                     "alg_bytes_per_launch": b / c, "peak_source": peak_src}
     tuples = (nr + ns) * world * cfg.get("dims", 1)
     value = tuples / (ms / 1e3)
@@ -426,14 +493,10 @@ def main():
     out = {
         "metric": METRIC, "value": value, "unit": "tuples/s", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u32",
+        "vs_baseline": None, "dtype": "u64" if cfg["key"] == 8 else "u32",
         "data": "synthetic: bit-identical to the reference's workloads::gen_pk_fk "
                 "(seed 42 + rank), generated on the device",
-        "config": {"workload": cfg["desc"] if a.scale_log2 == 0 else f"{a.config}/2^{a.scale_log2}",
-                   "variant": a.variant.upper(), "r_rows": nr, "s_rows": ns, "out_rows": rows,
-                   "l2": "inputs >> 126 MB L2 (no flush needed)" if nr >= 1 << 24
-                   else "inputs partly L2-resident (small config)",
-                   "parallelism": f"radix-sharded x{world}" if sharded else "single GPU"},
+        "config": config_dict(cfg, a, nr, ns, world), "out_rows": rows,
         "roofline": roofline,
         "join_roofline": {"b_alg_bytes": balg, "b_min_bytes": b_min(nr, ns, rows, kb, ws),
                           "frac_b_alg": balg / (ms / 1e3) / (peak * 1e9),
@@ -450,8 +513,6 @@ def main():
     }
     if shuffle_info:
         out["shuffle"] = shuffle_info
-        out["config"]["workload"] = (f"C5-shaped weak scaling: |R|={world}x2^27, |S|={world}x2^28 "
-                                     "total, 4-byte key + 2 x 4-byte payloads, cj_gen_shard")
     if rank == 0 and not sharded and not a.no_extras and a.config == "C2":
         # the other variants (3 timed steps each)
         var = {}
@@ -480,6 +541,10 @@ def main():
         # end to end through the host-buffer C-ABI (pinned host in/out)
         out["e2e"] = e2e_leg(ctx, R, S, opt, steps=a.e2e_steps)
         out["cpu_baseline"] = cpu_baseline(nr, ns, a.variant)
+        if not a.no_configs:
+            del Rc, Sc, R, S
+            torch.cuda.empty_cache()
+            out["configs"] = configs_leg(ctx, peak)
     if rank == 0:
         if out_fd is not None:
             sys.stdout.flush()
@@ -488,6 +553,52 @@ def main():
             print(json.dumps(out))
     if sharded:
         dist.destroy_process_group()
+
+
+def configs_leg(ctx, peak, names=("C3", "C4z0.5", "C4z1.0", "C4z1.5"), steps=3):
+    """The other full-size BASELINE.json configs (C3, C4 at three skews): PHJ- and
+    SMJ-GFTR, one warm-up + `steps` timed joins each, device-resident inputs
+    generated bit-identically to the reference; ms and fraction of B_alg."""
+    import ctypes as C
+    import torch
+    import paper_2312_00720_b200 as cj
+    from paper_2312_00720_b200 import _capi as A
+    L = A.lib()
+    res = A.JoinResult()
+    recs = {}
+    for name in names:
+        cfg = CONFIGS[name]
+        nr, ns = cfg["r"], cfg["s"]
+        R, S = gen_config(ctx, cfg, nr, ns)
+        Rc, Sc = cj.coljoin.c_relation(R), cj.coljoin.c_relation(S)
+        key_bits = max(1, (2 * nr - 1).bit_length() if cfg["match"] < 1 else (nr - 1).bit_length())
+        rec = {}
+        for v in ("phj-gftr", "smj-gftr"):
+            o = cj.options(*v.split("-"))
+
+            def one():
+                A.check(L.cj_run_join(ctx.h, C.byref(Rc), C.byref(Sc), C.byref(o), C.byref(res)),
+                        ctx.h, "run_join")
+                rows = res.rows
+                A.check(L.cj_result_free(ctx.h, C.byref(res)), ctx.h, "free")
+                return rows
+            rows = one()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(ctx.stream)
+            for _ in range(steps):
+                one()
+            e1.record(ctx.stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / steps
+            va, vp = v.split("-")
+            balg = b_alg(va, vp, nr, ns, rows, cfg["key"], cfg["widths"], key_bits)
+            rec[v] = {"ms": ms, "tuples_per_s": (nr + ns) / (ms / 1e3), "out_rows": rows,
+                      "frac_b_alg": balg / (ms / 1e3) / (peak * 1e9)}
+        recs[name] = {"workload": cfg["desc"], **rec}
+        del Rc, Sc, R, S
+        torch.cuda.empty_cache()
+    return recs
 
 
 def e2e_leg(ctx, R, S, opt, steps=32, streams=2):
