@@ -383,12 +383,15 @@ def main():
         # PK-FK join; rows are shuffled to their key's shard over NCCL
         from paper_2312_00720_b200 import distributed as D
         R, S = D.gen_shard(ctx, nr * world, ns * world, rank, world, NPAY, NPAY, SEED)
+        comm = D.Comm.from_group(ctx)
 
         def step():
             t = {}
-            out = D.distributed_join(ctx, R, S, algo, pattern, timings=t)
-            shuffle["exchange_ms"] += t["exchange_ms"]
-            shuffle["bytes"] += t["bytes_sent"]
+            out = D.distributed_join(ctx, R, S, algo, pattern, comm=comm, timings=t)
+            shuffle["exchange_ms"] += (t["exchange_r_ns"] + t["exchange_s_ns"]) / 1e6
+            shuffle["shard_ms"] = shuffle.get("shard_ms", 0.0) + t["shard_ns"] / 1e6
+            shuffle["bytes"] += t["bytes_sent_peers"]
+            shuffle["first_bits"] = t["first_bits"]
             rows = out.matches
             phases = (out.report.transform_ns, out.report.find_ns, out.report.materialize_ns)
             del out
@@ -421,15 +424,23 @@ def main():
     clk = clocks.stop()
     shuffle_info = None
     if sharded:
-        ex = torch.tensor([shuffle["exchange_ms"] / max(a.steps + a.warmup, 1)], device="cuda")
+        nsteps = max(a.steps + a.warmup, 1)
+        ex = torch.tensor([shuffle["exchange_ms"] / nsteps, shuffle.get("shard_ms", 0.0) / nsteps],
+                          device="cuda")
         dist.all_reduce(ex, op=dist.ReduceOp.MAX)
-        per_step_bytes = shuffle["bytes"] / max(a.steps + a.warmup, 1)
-        shuffle_info = {"bytes_sent_per_gpu_per_step": per_step_bytes,
-                        "exchange_ms_max_over_ranks": float(ex.item()),
-                        "nvlink_gbs_per_gpu": per_step_bytes / 1e9 / (float(ex.item()) / 1e3)
-                        if ex.item() > 0 else None,
+        per_step_bytes = shuffle["bytes"] / nsteps
+        ex_ms, sh_ms = float(ex[0].item()), float(ex[1].item())
+        shuffle_info = {"bytes_sent_to_peers_per_gpu_per_step": per_step_bytes,
+                        "exchange_ms_max_over_ranks": ex_ms,
+                        "shard_pass_ms_max_over_ranks": sh_ms,
+                        "first_lsd_bits_in_shard_pass": shuffle.get("first_bits"),
+                        "nvlink_gbs_per_gpu": per_step_bytes / 1e9 / (ex_ms / 1e3)
+                        if ex_ms > 0 and per_step_bytes > 0 else None,
                         "nvlink_peak_gbs_per_dir": 770.0,
-                        "transport": "NCCL all_to_all_single (torch.distributed, backend nccl)"}
+                        "how": "device time of the R and S data exchanges (CUDA events on the "
+                               "library's NCCL stream), bytes to other ranks only",
+                        "transport": "cj_run_join_sharded: grouped ncclSend/ncclRecv per (peer, "
+                                     "first-digit run), NCCL over NVLink/NVSwitch"}
     # Per-kernel CUDA-event records: the same K steps again, each kernel
     # bracketed by events on the ctx stream (the launching stream).  Kept out of
     # the headline region above; the event pool is reset per step so no event
@@ -552,6 +563,7 @@ def main():
         else:
             print(json.dumps(out))
     if sharded:
+        comm.close()
         dist.destroy_process_group()
 
 

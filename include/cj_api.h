@@ -262,6 +262,77 @@ int cj_shard_partition(cj_ctx* ctx, const void* keys_dev, void* keys_out_dev, ui
                        void* const* vals_out_dev, const uint32_t* val_bytes, uint32_t nvals,
                        uint64_t* counts_host);
 
+/* cj_shard_partition with the receiver's first LSD digit folded in: rows are
+ * stably grouped by digit = shard << first_bits | (key & (2^first_bits - 1)),
+ * i.e. by destination and, inside a destination, by the low first_bits key
+ * bits; counts_host[parts << first_bits] rows per digit (row-major
+ * [destination][low bits]).  parts << first_bits <= 256.  Rows wider than the
+ * staging allows go in column groups (same permutation). */
+int cj_shard_partition_ex(cj_ctx* ctx, const void* keys_dev, void* keys_out_dev, uint64_t n,
+                          uint32_t key_bytes, uint32_t parts, uint32_t first_bits,
+                          const void* const* vals_dev, void* const* vals_out_dev,
+                          const uint32_t* val_bytes, uint32_t nvals, uint64_t* counts_host);
+
+/* Placement of one all-to-all exchange of shard-grouped rows (host only, no
+ * device work).  send_counts[dst][d]: rows this rank sends to dst with low
+ * digit d (its cj_shard_partition_ex counts); recv_counts[src][d]: rows src
+ * sends here.  send_off[dst][d] = row offset of that run in the send layout;
+ * recv_off[src][d] = where src's digit-d run lands so that the received
+ * relation is stably grouped by d (runs of one digit in source-rank order):
+ * the first LSD pass of the local join is then already done.
+ * *recv_total = rows received. */
+int cj_exchange_plan(uint32_t world, uint32_t digits, const uint64_t* send_counts,
+                     const uint64_t* recv_counts, uint64_t* send_off, uint64_t* recv_off,
+                     uint64_t* recv_total);
+
+/* ---- NCCL communicator and the sharded join -------------- */
+/* NCCL is bound at run time (dlopen "libnccl.so.2": the copy a host process
+ * already loaded, e.g. torch's, else the system one); CJ_ERR_NCCL when absent. */
+#define CJ_COMM_ID_BYTES 128
+typedef struct cj_comm cj_comm;
+/* ncclGetUniqueId: rank 0 creates the id, the caller broadcasts the bytes. */
+int cj_comm_unique_id(uint8_t* id_out);
+/* One rank's communicator on ctx's device (ncclCommInitRank, plus a split
+ * control communicator for count exchanges that must not queue behind data). */
+int cj_comm_init(cj_ctx* ctx, const uint8_t* id, int nranks, int rank, cj_comm** out);
+int cj_comm_destroy(cj_comm* comm);
+int cj_comm_size(const cj_comm* comm);
+int cj_comm_rank(const cj_comm* comm);
+
+typedef struct {
+  uint32_t first_bits;              /* low key bits pre-sorted by the exchange */
+  uint64_t r_rows_received, s_rows_received;
+  uint64_t bytes_sent_peers;        /* to other ranks (self excluded), R + S */
+  uint64_t bytes_received_peers;
+  uint64_t shard_ns;                /* both shard partitions (device time, ctx stream) */
+  uint64_t exchange_r_ns, exchange_s_ns;  /* data exchanges (device time, comm stream) */
+  uint64_t wall_ns;                 /* the whole call, host clock */
+} cj_shuffle_stats;
+
+/* Shuffle one relation: shard partition (with the first digit), count
+ * exchange, grouped ncclSend/ncclRecv of every column into runs placed by
+ * cj_exchange_plan.  out receives library-allocated device columns (release
+ * with cj_relation_free); it is stably grouped by its low first_bits bits. */
+int cj_shuffle_relation(cj_ctx* ctx, cj_comm* comm, const cj_relation* in, uint32_t first_bits,
+                        cj_relation* out, cj_shuffle_stats* stats);
+int cj_relation_free(cj_ctx* ctx, cj_relation* rel);
+
+/* run_join on relations already stably grouped by their low presorted_bits
+ * key bits (what cj_shuffle_relation delivers): the first LSD pass of the
+ * transform is skipped.  Output multiset = cj_run_join's. */
+int cj_run_join_presorted(cj_ctx* ctx, const cj_relation* build, const cj_relation* probe,
+                          const cj_join_options* opt, uint32_t presorted_bits,
+                          cj_join_result* res);
+
+/* The radix-sharded join: every rank passes its slice of R and S; rows move to
+ * shard(key)'s rank (the shuffle above, R's exchange overlapping S's shard
+ * partition, S's overlapping R's local transform), and each rank joins its
+ * shard.  res = this rank's share of the output (the union over ranks is the
+ * join).  Collective: every rank of comm calls it with the same options. */
+int cj_run_join_sharded(cj_ctx* ctx, cj_comm* comm, const cj_relation* build,
+                        const cj_relation* probe, const cj_join_options* opt,
+                        cj_join_result* res, cj_shuffle_stats* stats);
+
 /* Weak-scaling shard generator: rank r of `ranks` gets |R|/ranks rows of a PK
  * domain that is a bijective scramble of [0, |R|) (|R| a power of two; a
  * 4-round Feistel permutation keyed by seed) and |S|/ranks uniform foreign

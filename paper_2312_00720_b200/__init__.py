@@ -12,7 +12,7 @@ from .coljoin import (Context, Relation, JoinOutput, PhaseReport, histogram,  # 
                       exclusive_prefix_sum, radix_partition, radix_partition_passes, sort_pairs,
                       sort_keys, gather, gather_clusteredness, partition_relation,
                       hash_find_matches, merge_find_matches, run_join, run_join_host,
-                      gen_pk_fk, to_device, to_host, options, run_join_sequence, gen_star,
+                      run_join_presorted, gen_pk_fk, to_device, to_host, options, run_join_sequence, gen_star,
                       SequenceStep, export_relation, import_relation)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

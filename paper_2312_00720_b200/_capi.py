@@ -82,6 +82,14 @@ class SequenceStep(C.Structure):
                 ("materialize_ns", C.c_uint64), ("fk_fetch_ns", C.c_uint64)]
 
 
+class ShuffleStats(C.Structure):
+    _fields_ = [("first_bits", C.c_uint32), ("r_rows_received", C.c_uint64),
+                ("s_rows_received", C.c_uint64), ("bytes_sent_peers", C.c_uint64),
+                ("bytes_received_peers", C.c_uint64), ("shard_ns", C.c_uint64),
+                ("exchange_r_ns", C.c_uint64), ("exchange_s_ns", C.c_uint64),
+                ("wall_ns", C.c_uint64)]
+
+
 class Partitioned(C.Structure):
     _fields_ = [("keys", C.c_void_p), ("offsets", C.c_void_p), ("carried", C.c_void_p),
                 ("rows", C.c_uint64)]
@@ -129,6 +137,23 @@ PROTOS = {
                                    C.POINTER(JoinResult), _U64P, _U64P]),
     "cj_shard_partition": (C.c_int, [_P, _P, _P, C.c_uint64, C.c_uint32, C.c_uint32, _PP, _PP,
                                      _U32P, C.c_uint32, _U64P]),
+    "cj_shard_partition_ex": (C.c_int, [_P, _P, _P, C.c_uint64, C.c_uint32, C.c_uint32,
+                                        C.c_uint32, _PP, _PP, _U32P, C.c_uint32, _U64P]),
+    "cj_exchange_plan": (C.c_int, [C.c_uint32, C.c_uint32, _U64P, _U64P, _U64P, _U64P, _U64P]),
+    "cj_comm_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
+    "cj_comm_init": (C.c_int, [_P, C.POINTER(C.c_uint8), C.c_int, C.c_int, C.POINTER(_P)]),
+    "cj_comm_destroy": (C.c_int, [_P]),
+    "cj_comm_size": (C.c_int, [_P]),
+    "cj_comm_rank": (C.c_int, [_P]),
+    "cj_shuffle_relation": (C.c_int, [_P, _P, C.POINTER(Relation), C.c_uint32,
+                                      C.POINTER(Relation), C.POINTER(ShuffleStats)]),
+    "cj_relation_free": (C.c_int, [_P, C.POINTER(Relation)]),
+    "cj_run_join_presorted": (C.c_int, [_P, C.POINTER(Relation), C.POINTER(Relation),
+                                        C.POINTER(JoinOptions), C.c_uint32,
+                                        C.POINTER(JoinResult)]),
+    "cj_run_join_sharded": (C.c_int, [_P, _P, C.POINTER(Relation), C.POINTER(Relation),
+                                      C.POINTER(JoinOptions), C.POINTER(JoinResult),
+                                      C.POINTER(ShuffleStats)]),
     "cj_gen_shard": (C.c_int, [_P, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
                                C.c_uint32, C.c_uint64, _P, _PP, _P, _PP]),
     "cj_set_kernel_timing": (C.c_int, [_P, C.c_int]),

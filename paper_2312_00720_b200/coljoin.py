@@ -356,14 +356,8 @@ def c_relation(rel: Relation, host: bool = False) -> A.Relation:
     return r
 
 
-def run_join(ctx: Context, build: Relation, probe: Relation, algo="phj", pattern="gftr",
-             **kw) -> JoinOutput:
-    """join_engine.hpp:68 run_join on device-resident relations."""
-    opt = options(algo, pattern, **kw)
-    R, S = c_relation(build), c_relation(probe)
-    res = A.JoinResult()
-    check(A.lib().cj_run_join(ctx.h, C.byref(R), C.byref(S), C.byref(opt), C.byref(res)),
-          ctx.h, "run_join")
+def join_output(ctx: Context, res, R, S, build: Relation, probe: Relation, kw) -> JoinOutput:
+    """Wrap a cj_join_result's library-owned columns as torch tensors."""
     t = res.rows
     key = _wrap(ctx, res.key, t, R.key_bytes)
     pays = [_wrap(ctx, res.pay[i], t, R.pay_bytes[i]) for i in range(R.npay)]
@@ -376,6 +370,30 @@ def run_join(ctx: Context, build: Relation, probe: Relation, algo="phj", pattern
                                         res.peak_materialize_b)), t,
                       res.clusteredness_r if kw.get("want_stats") else 1.0,
                       res.clusteredness_s if kw.get("want_stats") else 1.0, ids_r, ids_s)
+
+
+def run_join(ctx: Context, build: Relation, probe: Relation, algo="phj", pattern="gftr",
+             **kw) -> JoinOutput:
+    """join_engine.hpp:68 run_join on device-resident relations."""
+    opt = options(algo, pattern, **kw)
+    R, S = c_relation(build), c_relation(probe)
+    res = A.JoinResult()
+    check(A.lib().cj_run_join(ctx.h, C.byref(R), C.byref(S), C.byref(opt), C.byref(res)),
+          ctx.h, "run_join")
+    return join_output(ctx, res, R, S, build, probe, kw)
+
+
+def run_join_presorted(ctx: Context, build: Relation, probe: Relation, presorted_bits: int,
+                       algo="phj", pattern="gftr", **kw) -> JoinOutput:
+    """run_join on relations already stably grouped by their low
+    `presorted_bits` key bits (what the sharded join's exchange delivers): the
+    transform skips its first LSD pass; the output multiset is run_join's."""
+    opt = options(algo, pattern, **kw)
+    R, S = c_relation(build), c_relation(probe)
+    res = A.JoinResult()
+    check(A.lib().cj_run_join_presorted(ctx.h, C.byref(R), C.byref(S), C.byref(opt),
+                                        presorted_bits, C.byref(res)), ctx.h, "run_join_presorted")
+    return join_output(ctx, res, R, S, build, probe, kw)
 
 
 class _HostArena:

@@ -109,13 +109,12 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   return x ^ (x >> 31);
 }
 
-// Digit of a key: bits [shift, shift + log2(mask+1)) or, when hparts > 0, the
-// shard of the key, floor(mix64(key) * hparts / 2^64) — uncorrelated with the
-// low key bits that pick partitions and hash slots.
-template <class K>
-__device__ __forceinline__ uint32_t key_digit(K k, uint32_t shift, uint32_t mask, uint32_t hparts) {
-  if (hparts) return (uint32_t)__umul64hi(mix64((uint64_t)k), (uint64_t)hparts);
-  return (uint32_t)(k >> shift) & mask;
+// Shard digit of a key: shard = floor(mix64(key) * hparts / 2^64) —
+// uncorrelated with the low key bits that pick partitions and hash slots —
+// followed by the key's low `lowbits` bits (the receiver's first LSD digit).
+__device__ __forceinline__ uint32_t shard_digit(uint64_t k, uint32_t hparts, uint32_t lowbits) {
+  const uint32_t s = (uint32_t)__umul64hi(mix64(k), (uint64_t)hparts);
+  return (s << lowbits) | ((uint32_t)k & ((1u << lowbits) - 1u));
 }
 
 // ---- TMA bulk copies (cp.async.bulk) + mbarrier ----------------------------

@@ -5,6 +5,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <functional>
+#include <new>
+#include <stdexcept>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -109,6 +112,9 @@ struct ValCols {
 struct PassPlan {
   int npasses = 0;
   uint32_t lo[64] = {}, hi[64] = {};
+  int done = 0;  // leading passes the input already went through (a presorted
+                 // input: the sharded join's receivers get rows grouped by the
+                 // first digit); skipped, the rest run as usual
 };
 
 // Geometry of a blocked scatter pass: tile size (shared-memory budget), tile
@@ -131,14 +137,16 @@ ScatterGeom scatter_geom(cj_ctx* ctx, uint64_t n, int key_bytes, const ValCols& 
 // Per-block digit counts (cnt[b][p][256]) of every pass of `plan` (<= 8) in one
 // read of the keys, over the blocks of geometry g.
 void block_hist(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes, const PassPlan& plan,
-                const ScatterGeom& g, uint32_t* cnt_dev, uint32_t hparts = 0);
+                const ScatterGeom& g, uint32_t* cnt_dev, uint32_t hparts = 0,
+                uint32_t lowbits = 0);
 
 // block_hist + digit totals (totals_dev[p*256+d]) + exclusive digit bases
 // (base_dev[p*256+d]); totals_host after one host round trip when non-null.
 void histogram_passes(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes,
                       const PassPlan& plan, const ScatterGeom& g, uint32_t* cnt_dev,
                       uint32_t* totals_dev, uint64_t* base_dev,
-                      std::vector<uint32_t>* totals_host, uint32_t hparts = 0);
+                      std::vector<uint32_t>* totals_host, uint32_t hparts = 0,
+                      uint32_t lowbits = 0);
 
 // One stable scatter pass.  With per-block counts of this pass (cnt, stride
 // cnt_stride) and a TMA-eligible geometry it runs the blocked kernel (no
@@ -146,12 +154,14 @@ void histogram_passes(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes,
 void scatter_pass(cj_ctx* ctx, const void* keys_in, void* keys_out, uint64_t n, int key_bytes,
                   uint32_t lo, uint32_t hi, const uint64_t* base_dev, const uint32_t* cnt,
                   uint32_t cnt_stride, const ScatterGeom& g, const ValCols& vals,
-                  uint32_t hparts = 0);
+                  uint32_t hparts = 0, uint32_t lowbits = 0);
 
-// Stable partition of rows by shard = floor(mix64(key) * parts / 2^64) (the
-// multi-GPU shuffle's send layout); counts_host[parts] rows per shard.
+// Stable partition of rows by digit = shard << lowbits | (key & (2^lowbits - 1)),
+// shard = floor(mix64(key) * parts / 2^64) (the multi-GPU shuffle's send
+// layout: by destination, then by the receiver's first LSD digit);
+// counts_host[parts << lowbits] rows per digit.
 void shard_partition(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, int key_bytes,
-                     uint32_t parts, const ValCols& vals, uint64_t* counts_host);
+                     uint32_t parts, uint32_t lowbits, const ValCols& vals, uint64_t* counts_host);
 
 // Stable LSD over the plan; constant-digit passes skipped; the last executed
 // pass lands in the caller's outputs.  gen_ids handled in the first pass.
@@ -235,6 +245,43 @@ void gen_star(cj_ctx* ctx, uint64_t fact_rows, uint32_t dims, uint64_t dim_rows,
 void gen_shard(cj_ctx* ctx, uint64_t r_total, uint64_t s_total, uint32_t rank, uint32_t ranks,
                uint32_t r_pay, uint32_t s_pay, uint64_t seed, void* r_key, void* const* r_pays,
                void* s_key, void* const* s_pays);
+
+// ---- engine.cu ------------------------------------------------------------------
+// Optional hooks of run_join_dev (the sharded join's receivers).
+struct JoinHooks {
+  // both sides arrive stably grouped by their low `presorted_bits` key bits:
+  // the transform skips that first LSD pass
+  unsigned presorted_bits = 0;
+  // called (host side) before side 0 (build) / 1 (probe) is first read on the
+  // ctx stream: the sharded join makes the stream wait for that side's exchange
+  std::function<void(int)> before_side;
+};
+void run_join_dev(cj_ctx* ctx, const cj_relation* R, const cj_relation* S,
+                  const cj_join_options* opt, cj_join_result* res,
+                  const JoinHooks* hooks = nullptr);
+void alloc_output(cj_ctx* ctx, const cj_relation* r, const cj_relation* s, uint64_t cap,
+                  bool ids, cj_join_result* res);
+void free_output(cj_ctx* ctx, cj_join_result* res);
+unsigned default_total_radix_bits(uint64_t build_rows);
+void validate_relation(const cj_relation* r, const char* what);
+
+// Runs fn, mapping exceptions to status codes (the C boundary).
+template <class F>
+int guarded(cj_ctx* ctx, F&& fn) {
+  try {
+    fn();
+    return CJ_OK;
+  } catch (const Error& e) {
+    if (ctx) ctx->last_error = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    if (ctx) ctx->last_error = "host allocation failed";
+    return CJ_ERR_OUT_OF_MEMORY;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->last_error = e.what();
+    return CJ_ERR_CUDA;
+  }
+}
 
 // error word helpers: kernels OR codes into ctx->err_word; raise after sync
 enum : uint32_t { kErrOOB = 1u, kErrOverflow = 2u, kErrNotSorted = 4u, kErrDupKeys = 8u };

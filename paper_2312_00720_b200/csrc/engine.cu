@@ -72,9 +72,7 @@ void raise_device_errors(cj_ctx* ctx) {
   if (e & dev::kErrStall) fail(CJ_ERR_CUDA, "decoupled look-back stalled (internal error)");
 }
 
-namespace {
-
-__global__ void k_abs_diff_sum(const uint32_t* __restrict__ ids, uint64_t n,
+static __global__ void k_abs_diff_sum(const uint32_t* __restrict__ ids, uint64_t n,
                                unsigned long long* out) {
   uint64_t acc = 0;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x + 1; i < n;
@@ -147,6 +145,32 @@ PassPlan device_plan(unsigned total_bits, unsigned per_pass) {
   return p;
 }
 
+// Plan for an input already stably grouped by its low `f` key bits (the
+// sharded join's received rows): pass [0, f) is marked done, the remaining
+// bits [f, total) run in balanced passes of at most `max_w` bits (and at least
+// ceil(rest / per_pass) of them).  Same stable layout as the full plan.
+PassPlan presorted_plan(unsigned total_bits, unsigned f, unsigned max_w, unsigned per_pass) {
+  if (f > total_bits) f = total_bits;
+  PassPlan p;
+  p.npasses = 1;
+  p.lo[0] = 0;
+  p.hi[0] = f;
+  p.done = 1;
+  const unsigned rest = total_bits - f;
+  if (rest == 0) return p;
+  unsigned np = std::max((rest + per_pass - 1) / per_pass, (rest + max_w - 1) / max_w);
+  np = std::min(np, rest);
+  unsigned lo = f;
+  for (unsigned i = 0; i < np && p.npasses < CJ_MAX_PASSES * 3; ++i) {
+    const unsigned w = (total_bits - lo + (np - i) - 1) / (np - i);
+    p.lo[p.npasses] = lo;
+    p.hi[p.npasses] = lo + w;
+    ++p.npasses;
+    lo += w;
+  }
+  return p;
+}
+
 void check_key_bytes(uint32_t kb) {
   if (kb != 4 && kb != 8) fail(CJ_ERR_KIND, "key must be a 4- or 8-byte integer column");
 }
@@ -164,6 +188,7 @@ void lsd_any(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, int kb,
   for (int s = 0; s < plan.npasses; s += CJ_MAX_PASSES) {
     PassPlan seg;
     seg.npasses = std::min(CJ_MAX_PASSES, plan.npasses - s);
+    seg.done = std::max(0, std::min(plan.done - s, seg.npasses));
     for (int i = 0; i < seg.npasses; ++i) {
       seg.lo[i] = plan.lo[s + i];
       seg.hi[i] = plan.hi[s + i];
@@ -211,7 +236,7 @@ void validate_relation(const cj_relation* r, const char* what) {
 // Transform one side: partition (PHJ) or sort (SMJ) the key with the carried
 // columns.  gfur: carried = generated ids; gftr: carried = every payload.
 Side transform(cj_ctx* ctx, const cj_relation* rel, int algo, bool gfur, unsigned total_bits,
-               unsigned bits_per_pass, std::vector<void*>& owned) {
+               unsigned bits_per_pass, std::vector<void*>& owned, unsigned presorted = 0) {
   Side s;
   const uint64_t n = rel->rows;
   const int kb = (int)rel->key_bytes;
@@ -241,14 +266,23 @@ Side transform(cj_ctx* ctx, const cj_relation* rel, int algo, bool gfur, unsigne
     ~LiveScope() { c->assume_live_passes = false; }
   } live_scope(ctx);
   if (algo == CJ_SMJ) {
-    lsd_any(ctx, rel->key, s.keys, n, kb, sort_plan(ctx, rel->key, n, kb, v), v);
+    PassPlan plan = sort_plan(ctx, rel->key, n, kb, v);
+    if (presorted > 0) {  // keys above bit B are zero: sorted by [0, f >= B) is sorted
+      const unsigned bits = plan.npasses ? plan.hi[plan.npasses - 1] : 0;
+      plan = presorted_plan(bits, std::min(presorted, bits), 8, 8);
+    }
+    lsd_any(ctx, rel->key, s.keys, n, kb, plan, v);
   } else {
     s.offsets = static_cast<uint64_t*>(ctx->alloc(sizeof(uint64_t) * ((1ull << total_bits) + 1)));
     owned.push_back(s.offsets);
     if (total_bits == 0) {
       copy_columns(ctx, rel->key, s.keys, n, kb, v);
     } else {
-      lsd_any(ctx, rel->key, s.keys, n, kb, device_plan(total_bits, bits_per_pass), v);
+      // a hint wider than the partition bits says nothing about them
+      lsd_any(ctx, rel->key, s.keys, n, kb,
+              presorted > 0 && presorted <= total_bits
+                  ? presorted_plan(total_bits, presorted, 6, bits_per_pass)
+                  : device_plan(total_bits, bits_per_pass), v);
     }
     partition_offsets(ctx, s.keys, n, kb, total_bits, s.offsets);
   }
@@ -294,7 +328,8 @@ struct PhasePeaks {
 };
 
 void run_join_dev(cj_ctx* ctx, const cj_relation* R, const cj_relation* S,
-                  const cj_join_options* opt, cj_join_result* res) {
+                  const cj_join_options* opt, cj_join_result* res, const JoinHooks* hooks) {
+  const unsigned presorted = hooks ? hooks->presorted_bits : 0;
   validate_relation(R, "a build relation");
   validate_relation(S, "a probe relation");
   if (R->key_bytes != S->key_bytes) fail(CJ_ERR_KIND, "build and probe key kinds differ");
@@ -333,6 +368,10 @@ void run_join_dev(cj_ctx* ctx, const cj_relation* R, const cj_relation* S,
   PhasePeaks peaks(ctx);
   if (opt->algo == CJ_NPHJ) {
     // No transform: the build relation is hashed as is (nphj.cu).
+    if (hooks && hooks->before_side) {
+      hooks->before_side(0);
+      hooks->before_side(1);
+    }
     tm.mark(0);
     tm.mark(1);
     res->peak_transform_b = peaks.next();
@@ -415,8 +454,12 @@ void run_join_dev(cj_ctx* ctx, const cj_relation* R, const cj_relation* S,
 
   // ---- transform ----------------------------------------------------------
   tm.mark(0);
-  Side tr = transform(ctx, R, opt->algo, gfur, total_bits, opt->radix_bits_per_pass, owned);
-  Side ts = transform(ctx, S, opt->algo, gfur, total_bits, opt->radix_bits_per_pass, owned);
+  if (hooks && hooks->before_side) hooks->before_side(0);
+  Side tr = transform(ctx, R, opt->algo, gfur, total_bits, opt->radix_bits_per_pass, owned,
+                      presorted);
+  if (hooks && hooks->before_side) hooks->before_side(1);
+  Side ts = transform(ctx, S, opt->algo, gfur, total_bits, opt->radix_bits_per_pass, owned,
+                      presorted);
   tm.mark(1);
   res->peak_transform_b = peaks.next();
 
@@ -541,25 +584,6 @@ void run_join_dev(cj_ctx* ctx, const cj_relation* R, const cj_relation* S,
   }
 }
 
-// Runs fn, mapping exceptions to status codes (the C boundary).
-template <class F>
-int guarded(cj_ctx* ctx, F&& fn) {
-  try {
-    fn();
-    return CJ_OK;
-  } catch (const Error& e) {
-    if (ctx) ctx->last_error = e.msg;
-    return e.code;
-  } catch (const std::bad_alloc&) {
-    if (ctx) ctx->last_error = "host allocation failed";
-    return CJ_ERR_OUT_OF_MEMORY;
-  } catch (const std::exception& e) {
-    if (ctx) ctx->last_error = e.what();
-    return CJ_ERR_CUDA;
-  }
-}
-
-}  // namespace
 }  // namespace cj
 
 // ---- cj_ctx -------------------------------------------------------------------
@@ -1009,6 +1033,21 @@ int cj_run_join(cj_ctx* ctx, const cj_relation* build, const cj_relation* probe,
   });
 }
 
+int cj_run_join_presorted(cj_ctx* ctx, const cj_relation* build, const cj_relation* probe,
+                          const cj_join_options* opt, uint32_t presorted_bits,
+                          cj_join_result* res) {
+  return cj::guarded(ctx, [&] {
+    cj::JoinHooks h;
+    h.presorted_bits = presorted_bits;
+    try {
+      cj::run_join_dev(ctx, build, probe, opt, res, &h);
+    } catch (...) {
+      cj::free_output(ctx, res);
+      throw;
+    }
+  });
+}
+
 int cj_run_join_sequence(cj_ctx* ctx, const cj_relation* fact, const cj_relation* dims,
                          uint32_t n_dims, const cj_join_options* opt, cj_sequence_step* steps,
                          cj_join_result* last) {
@@ -1233,7 +1272,18 @@ int cj_shard_partition(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n
   return cj::guarded(ctx, [&] {
     cj::check_key_bytes(kb);
     cj::ValCols v = make_vals(vin, vout, vbytes, nvals, 0);
-    cj::shard_partition(ctx, keys, keys_out, n, (int)kb, parts, v, counts_host);
+    cj::shard_partition(ctx, keys, keys_out, n, (int)kb, parts, 0, v, counts_host);
+  });
+}
+
+int cj_shard_partition_ex(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, uint32_t kb,
+                          uint32_t parts, uint32_t first_bits, const void* const* vin,
+                          void* const* vout, const uint32_t* vbytes, uint32_t nvals,
+                          uint64_t* counts_host) {
+  return cj::guarded(ctx, [&] {
+    cj::check_key_bytes(kb);
+    cj::ValCols v = make_vals(vin, vout, vbytes, nvals, 0);
+    cj::shard_partition(ctx, keys, keys_out, n, (int)kb, parts, first_bits, v, counts_host);
   });
 }
 

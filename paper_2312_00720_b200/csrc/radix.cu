@@ -42,6 +42,7 @@ constexpr int kHistSub = 4;  // CTAs per static block in the counting kernel
 struct HistArgs {
   uint64_t n, tile, tiles;
   uint32_t nblocks, hparts;
+  uint32_t lowbits;  // shard mode: digit = shard << lowbits | low key bits
   uint32_t shift[8], mask[8];
 };
 
@@ -82,7 +83,7 @@ k_block_hist(const K* __restrict__ keys, const __grid_constant__ HistArgs a,
   }
   auto count = [&](K k) {
     if (SHARD) {
-      atomicAdd(&mine[(uint32_t)__umul64hi(dev::mix64((uint64_t)k), (uint64_t)a.hparts)], 1u);
+      atomicAdd(&mine[dev::shard_digit((uint64_t)k, a.hparts, a.lowbits)], 1u);
     } else {
 #pragma unroll
       for (int p = 0; p < NP; ++p) atomicAdd(&mine[p * kR + ((uint32_t)(k >> shf[p]) & msk[p])], 1u);
@@ -136,7 +137,7 @@ void launch_hist(cj_ctx* ctx, const K* keys, const HistArgs& a, uint32_t* cnt) {
 
 template <class K, int RB>
 void launch_hist_np(cj_ctx* ctx, const K* keys, const HistArgs& a, int np, uint32_t* cnt) {
-  if (a.hparts) return launch_hist<K, 1, true, 8>(ctx, keys, a, cnt);
+  if (a.hparts) return launch_hist<K, 1, true, RB>(ctx, keys, a, cnt);
   switch (np) {
     case 1: return launch_hist<K, 1, false, RB>(ctx, keys, a, cnt);
     case 2: return launch_hist<K, 2, false, RB>(ctx, keys, a, cnt);
@@ -389,7 +390,8 @@ struct BlockPassArgs {
   uint64_t n, tiles;
   uint32_t nblocks;
   uint32_t shift, mask, bits;
-  uint32_t hparts;          // > 0: digit = shard of the key (key_digit)
+  uint32_t hparts;          // > 0: digit = shard of the key << lowbits | its low lowbits bits
+  uint32_t lowbits;
   const uint64_t* base;     // [256] exclusive digit base of this pass
   const uint32_t* cnt;      // per-block counts of this pass: cnt[b * cnt_stride + d]
   uint32_t cnt_stride;
@@ -473,7 +475,7 @@ __device__ unsigned long long g_phase_clk[16];
 // Digit of key k in pass (shift, mask) or, in shard mode, its shard.
 template <bool SHARD, class K>
 __device__ __forceinline__ uint32_t digit_of(K k, const BlockPassArgs& a) {
-  if (SHARD) return (uint32_t)__umul64hi(dev::mix64((uint64_t)k), (uint64_t)a.hparts);
+  if (SHARD) return dev::shard_digit((uint64_t)k, a.hparts, a.lowbits);
   return (uint32_t)(k >> a.shift) & a.mask;
 }
 
@@ -783,7 +785,7 @@ k_scatter_v2(const __grid_constant__ BlockPassArgs a) {
 
 template <class K, int ITEMS, int RANK, int MINB, int RB>
 void launch_v2(cj_ctx* ctx, const BlockPassArgs& a, size_t smem) {
-  auto kern = a.hparts ? k_scatter_v2<K, ITEMS, RANK, true, MINB, 8>
+  auto kern = a.hparts ? k_scatter_v2<K, ITEMS, RANK, true, MINB, RB>
                        : k_scatter_v2<K, ITEMS, RANK, false, MINB, RB>;
   CJ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<a.nblocks, kTmaThreads, smem, ctx->stream>>>(a);
@@ -817,6 +819,7 @@ void launch_v2_items(cj_ctx* ctx, const BlockPassArgs& a, size_t smem, int items
     default: launch_v2<K, 4, RANK, 1, 8>(ctx, a, smem); break;
   }
 }
+
 
 template <class T>
 __global__ void k_iota(T* out, uint64_t n) {
@@ -885,7 +888,7 @@ ScatterGeom scatter_geom(cj_ctx* ctx, uint64_t n, int key_bytes, const ValCols& 
 }
 
 void block_hist(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes, const PassPlan& plan,
-                const ScatterGeom& g, uint32_t* cnt_dev, uint32_t hparts) {
+                const ScatterGeom& g, uint32_t* cnt_dev, uint32_t hparts, uint32_t lowbits) {
   const int np = plan.npasses;
   if (np < 1 || np > 8) fail(CJ_ERR_UNSUPPORTED, "histogram of 1..8 passes");
   HistArgs a{};
@@ -894,6 +897,7 @@ void block_hist(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes, const 
   a.tiles = g.tiles;
   a.nblocks = g.nblocks;
   a.hparts = hparts;
+  a.lowbits = lowbits;
   for (int p = 0; p < np; ++p) {
     a.shift[p] = plan.lo[p];
     a.mask[p] = (1u << (plan.hi[p] - plan.lo[p])) - 1u;
@@ -920,10 +924,10 @@ void block_hist(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes, const 
 void histogram_passes(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes,
                       const PassPlan& plan, const ScatterGeom& g, uint32_t* cnt_dev,
                       uint32_t* totals_dev, uint64_t* base_dev,
-                      std::vector<uint32_t>* totals_host, uint32_t hparts) {
+                      std::vector<uint32_t>* totals_host, uint32_t hparts, uint32_t lowbits) {
   const int np = plan.npasses;
   if (np > 8) fail(CJ_ERR_UNSUPPORTED, "histogram of more than 8 passes");
-  block_hist(ctx, keys, n, key_bytes, plan, g, cnt_dev, hparts);
+  block_hist(ctx, keys, n, key_bytes, plan, g, cnt_dev, hparts, lowbits);
   const uint32_t R = 1u << g.rb;
   ctx->kbegin("digit_bases", 12ull * R * np);
   k_digit_bases<<<1, 1024, 0, ctx->stream>>>(cnt_dev, g.nblocks, np, R, totals_dev, base_dev);
@@ -940,9 +944,12 @@ void histogram_passes(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes,
 
 void scatter_pass(cj_ctx* ctx, const void* keys_in, void* keys_out, uint64_t n, int key_bytes,
                   uint32_t lo, uint32_t hi, const uint64_t* base_dev, const uint32_t* cnt,
-                  uint32_t cnt_stride, const ScatterGeom& g, const ValCols& vals, uint32_t hparts) {
+                  uint32_t cnt_stride, const ScatterGeom& g, const ValCols& vals, uint32_t hparts,
+                  uint32_t lowbits) {
   if (n == 0) return;
-  if (hparts && !(g.tma && cnt)) fail(CJ_ERR_UNSUPPORTED, "shard partition needs aligned columns");
+  if (hparts && !g.tma)
+    fail(CJ_ERR_UNSUPPORTED, "shard partition needs 16-byte aligned columns");
+  if (hparts && !cnt) fail(CJ_ERR_UNSUPPORTED, "shard partition needs per-block counts");
   uint64_t row = key_bytes, wrow = key_bytes;
   for (int c = 0; c < vals.n; ++c) {
     row += vals.bytes[c] - ((vals.gen_ids && c == 0) ? 4 : 0);
@@ -959,6 +966,12 @@ void scatter_pass(cj_ctx* ctx, const void* keys_in, void* keys_out, uint64_t n, 
     a.bits = hi - lo;
     a.mask = (1u << (hi - lo)) - 1u;
     a.hparts = hparts;
+    a.lowbits = lowbits;
+    if (hparts) {  // digit = shard << lowbits | low bits: ceil(log2 parts) + lowbits bits
+      uint32_t sb = 0;
+      while ((1u << sb) < hparts) ++sb;
+      a.bits = sb + lowbits;
+    }
     a.base = base_dev;
     a.cnt = cnt;
     a.cnt_stride = cnt_stride;
@@ -1101,7 +1114,7 @@ void lsd_partition_group(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t
   if (counts_out) *counts_out = totals;
   std::vector<int> live;
   for (int p = 0; p < np; ++p) {
-    if (plan.hi[p] == plan.lo[p]) continue;
+    if (plan.hi[p] == plan.lo[p] || p < plan.done) continue;
     bool constant = n == 0;
     for (uint32_t d = 0; d < kRadix && !constant && !skip_check; ++d)
       if (totals[(size_t)p * kRadix + d] == n) constant = true;
@@ -1167,25 +1180,55 @@ void lsd_partition_group(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t
 
 }  // namespace
 
+// Stable partition by (shard, low `lowbits` key bits): the send layout of the
+// multi-GPU shuffle, grouped by destination and, inside a destination, by the
+// receiver's first LSD digit.  Rows wider than the TMA stage allows are
+// partitioned in column groups (each group with the key: the digits are the
+// same, so every group gets the same stable permutation).
 void shard_partition(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, int key_bytes,
-                     uint32_t parts, const ValCols& vals, uint64_t* counts_host) {
+                     uint32_t parts, uint32_t lowbits, const ValCols& vals, uint64_t* counts_host) {
   if (parts == 0 || parts > 256) fail(CJ_ERR_SPEC_INVALID, "shard count must be in [1, 256]");
-  uint32_t bits = 0;
-  while ((1u << bits) < parts) ++bits;
+  if (lowbits > 8 || ((uint64_t)parts << lowbits) > 256)
+    fail(CJ_ERR_FANOUT_TOO_LARGE, "shards x 2^first_bits must not exceed 256 digits");
+  const uint32_t digits = parts << lowbits;
   PassPlan plan;
   plan.npasses = 1;
   plan.lo[0] = 0;
-  plan.hi[0] = std::max(bits, 1u);
-  const ScatterGeom g = scatter_geom(ctx, n, key_bytes, vals, keys);
-  Scratch cnt(ctx, sizeof(uint32_t) * kRadix * g.nblocks), tot(ctx, sizeof(uint32_t) * kRadix),
-      base(ctx, sizeof(uint64_t) * kRadix);
+  plan.hi[0] = 8;
+  constexpr uint32_t kGroupBytes = 32;
+  std::vector<ValCols> groups;
+  {
+    ValCols cur;
+    uint32_t bytes = 0;
+    for (int c = 0; c < vals.n; ++c) {
+      if (cur.n > 0 && bytes + vals.bytes[c] > kGroupBytes) {
+        groups.push_back(cur);
+        cur = ValCols();
+        bytes = 0;
+      }
+      cur.in[cur.n] = vals.in[c];
+      cur.out[cur.n] = vals.out[c];
+      cur.bytes[cur.n] = vals.bytes[c];
+      ++cur.n;
+      bytes += vals.bytes[c];
+    }
+    groups.push_back(cur);
+  }
   std::vector<uint32_t> totals;
-  histogram_passes(ctx, keys, n, key_bytes, plan, g, cnt.as<uint32_t>(), tot.as<uint32_t>(),
-                   base.as<uint64_t>(), &totals, parts);
-  if (n > 0)
-    scatter_pass(ctx, keys, keys_out, n, key_bytes, 0, plan.hi[0], base.as<uint64_t>(),
-                 cnt.as<uint32_t>(), kRadix, g, vals, parts);
-  for (uint32_t d = 0; d < parts; ++d) counts_host[d] = totals[d];
+  // up to 64 digits: 64-entry digit tables (longer tiles fit), else 256
+  const int rb = digits <= 64 ? 6 : 8;
+  for (size_t gi = 0; gi < groups.size(); ++gi) {
+    const ScatterGeom g = scatter_geom(ctx, n, key_bytes, groups[gi], keys, rb);
+    if (!g.tma) fail(CJ_ERR_UNSUPPORTED, "shard partition needs 16-byte aligned columns");
+    Scratch cnt(ctx, sizeof(uint32_t) * kRadix * g.nblocks), tot(ctx, sizeof(uint32_t) * kRadix),
+        base(ctx, sizeof(uint64_t) * kRadix);
+    histogram_passes(ctx, keys, n, key_bytes, plan, g, cnt.as<uint32_t>(), tot.as<uint32_t>(),
+                     base.as<uint64_t>(), gi == 0 ? &totals : nullptr, parts, lowbits);
+    if (n > 0)
+      scatter_pass(ctx, keys, keys_out, n, key_bytes, 0, 8, base.as<uint64_t>(),
+                   cnt.as<uint32_t>(), 1u << g.rb, g, groups[gi], parts, lowbits);
+  }
+  for (uint32_t d = 0; d < digits; ++d) counts_host[d] = n ? totals[d] : 0;
   CJ_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 

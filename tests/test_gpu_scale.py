@@ -79,7 +79,7 @@ def test_c2_generator_matches_reference(c2, golden):
 
 
 @pytest.mark.parametrize("algo,pattern", [("phj", "gftr"), ("smj", "gftr"), ("phj", "gfur"),
-                                          ("smj", "gfur"), ("nphj", "gftr")])
+                                          ("smj", "gfur"), ("nphj", "gftr"), ("nphj", "gfur")])
 def test_c2_join_digest_matches_reference(c2, algo, pattern):
     ctx, R, S = c2
     out = cj.run_join(ctx, R, S, algo, pattern)
@@ -109,33 +109,46 @@ def test_star3_chain_matches_reference(golden):
     ctx.close()
 
 
-@pytest.mark.parametrize("name,key,widths,match,zipf", [
-    ("C3", 8, (4, 8, 4, 8), 0.5, 0.0),
-    ("C4z1.5", 4, (4, 4), 1.0, 1.5),
-])
-def test_full_size_variants_agree(name, key, widths, match, zipf):
-    """BASELINE.json configs[2] / [3] at full size: no reference digest exists at
-    this scale (the host canonicalisation takes hours), so — as the reference's
-    own acceptance criterion 2 does (tests/acceptance_main.cpp:182-207) — every
-    variant must produce the same canonical rows; the small-scale shapes of
-    both configs are pinned to the reference by the golden cells."""
+FULL = {  # BASELINE.json configs[2] and [3] at full size (bench.py CONFIGS)
+    "C3": (8, (4, 8, 4, 8), 0.5, 0.0),
+    "C4z0.5": (4, (4, 4), 1.0, 0.5),
+    "C4z1.0": (4, (4, 4), 1.0, 1.0),
+    "C4z1.5": (4, (4, 4), 1.0, 1.5),
+}
+
+
+@pytest.mark.parametrize("name", sorted(FULL))
+def test_full_size_digest_matches_reference(name, golden):
+    """configs[2] (C3) and configs[3] (C4 at z = 0.5 / 1.0 / 1.5) at full size:
+    every variant's canonical digest equals the one the unmodified reference
+    computed for the same seed-42 workload (tests/golden/make_golden.py --full,
+    refjoin with its canonical rows, oracle.cpp:77-88), and so does the row
+    count.  NPHJ (no reference counterpart) must give the same rows."""
     import torch
+    g = [x for x in golden.get("full", []) if x["cell"]["name"] == name]
+    if not g:
+        pytest.skip(f"no full-size golden for {name} (make_golden.py --full {name})")
+    ref = g[0]["variants"]
+    digests = {v["digest"] for v in ref.values()}
+    assert len(digests) == 1  # the reference's four variants agree
+    want_digest = digests.pop()
+    want_rows = {v["rows_out"] for v in ref.values()}.pop()
+    key, widths, match, zipf = FULL[name]
     ctx = cj.Context(0)
     pb = 8 if 8 in widths else 4
     R, S = cj.gen_pk_fk(ctx, 1 << 27, 1 << 28, len(widths), len(widths), key, pb, match, zipf, 42)
-    if pb == 8:
+    if pb == 8:  # mixed widths: generated as u64, the 4-byte columns truncated (refjoin --widths)
         def narrow(cols):
             return [c if w == 8 else c.view(torch.int32)[::2].contiguous()
                     for c, w in zip(cols, widths)]
         R = cj.Relation(R.key, narrow(R.payloads), "R", True)
         S = cj.Relation(S.key, narrow(S.payloads), "S", False)
-    digests, rows = {}, set()
-    for algo, pattern in (("phj", "gftr"), ("smj", "gftr"), ("phj", "gfur"), ("nphj", "gftr")):
+    for algo, pattern in (("phj", "gftr"), ("smj", "gftr"), ("phj", "gfur"), ("smj", "gfur"),
+                          ("nphj", "gftr")):
         out = cj.run_join(ctx, R, S, algo, pattern)
-        rows.add(out.matches)
-        digests[(algo, pattern)] = canonical_digest_device([out.relation.key] +
-                                                           list(out.relation.payloads))
+        assert out.matches == want_rows, (algo, pattern)
+        assert canonical_digest_device([out.relation.key] + list(out.relation.payloads)) == \
+            want_digest, (algo, pattern)
         del out
-    assert len(rows) == 1 and len(set(digests.values())) == 1, (rows, digests)
     del R, S
     ctx.close()
