@@ -578,6 +578,10 @@ def configs_leg(ctx, peak, names=("C3", "C4z0.5", "C4z1.0", "C4z1.5"), steps=3):
     L = A.lib()
     res = A.JoinResult()
     recs = {}
+    # a fresh ctx (its own stream-ordered pool): the headline ctx's pool is
+    # fragmented by the variants and the e2e lanes, and a C3-sized reservation
+    # next to it can fall back to mapping memory mid-join
+    ctx = cj.Context(ctx.device)
     for name in names:
         cfg = CONFIGS[name]
         nr, ns = cfg["r"], cfg["s"]
@@ -610,6 +614,7 @@ def configs_leg(ctx, peak, names=("C3", "C4z0.5", "C4z1.0", "C4z1.5"), steps=3):
         recs[name] = {"workload": cfg["desc"], **rec}
         del Rc, Sc, R, S
         torch.cuda.empty_cache()
+    ctx.close()
     return recs
 
 

@@ -130,6 +130,7 @@ struct ScatterGeom {
   int ctas_per_sm = 2, stages = 2;
   int rank = 0;      // in-warp peer search: 0 atomic-OR masks, 1 ballots
   int rb = 8;        // digit bits of the passes (8, or 9 for wide full-width sorts)
+  int threads = 512; // per CTA (256: two CTAs per SM)
 };
 ScatterGeom scatter_geom(cj_ctx* ctx, uint64_t n, int key_bytes, const ValCols& vals,
                          const void* keys_in, int rb = 8);

@@ -249,8 +249,7 @@ __global__ void __launch_bounds__(kThreads) k_phj_find(const __grid_constant__ F
     if (u >= total_units) break;
     const uint64_t b_lo = s_b_lo, q_lo = s_q_lo;
     const uint32_t nb = (uint32_t)(s_b_hi - b_lo), nq = (uint32_t)(s_q_hi - q_lo);
-    uint32_t cap_log2 = 1;
-    while ((1u << cap_log2) < 2 * nb) ++cap_log2;
+    const uint32_t cap_log2 = nb <= 1 ? 1u : 33u - (uint32_t)__clz(nb - 1);
     const uint32_t cap = 1u << cap_log2, cmask = cap - 1;
 
     // 1. stage build keys (+ transformed R payloads) and clear the table
@@ -749,8 +748,8 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
       sync_c();  // res / list are rewritten by the next unit
       continue;
     }
-    uint32_t cap_log2 = 1;
-    while ((1u << cap_log2) < 2 * nb) ++cap_log2;
+    // smallest power of two >= 2 nb (at least 2)
+    const uint32_t cap_log2 = nb <= 1 ? 1u : 33u - (uint32_t)__clz(nb - 1);
     const uint32_t cap = 1u << cap_log2, cmask = cap - 1;
     if (!reuse) {
       if (tid == 0) s_dup = 0;
@@ -806,7 +805,50 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
     // 2. probe from shared memory; warp w owns a contiguous run of rounds
     uint32_t wcount = 0;  // <= qchunk per unit
     uint16_t* const me_out = !WRITE && a.match_e ? a.match_e + inf.q_lo : nullptr;
-    for (uint32_t r = r0; r < r1; ++r) {
+    uint32_t r = r0;
+    if (!has_dup) {
+      // four rounds at a time: the first table probe and the build-key check of
+      // every round are independent loads (collisions take the loop)
+      for (; r + 4 <= r1; r += 4) {
+        K key[4];
+        uint32_t sl[4], e[4];
+        bool in[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t jl = (r + u) * 32 + lane;
+          in[u] = jl < nq;
+          key[u] = in[u] ? pk[jl] : K(0);
+          sl[u] = slot_of(key[u], cap_log2);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) e[u] = tab[sl[u]];
+        K bkey[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) bkey[u] = e[u] != kNoMatch ? bk[e[u]] : K(0);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (!in[u]) continue;
+          const uint32_t jl = (r + u) * 32 + lane;
+          uint32_t out = kNoMatch, m = 0;
+          uint32_t ee = e[u], ss = sl[u];
+          K bb = bkey[u];
+          while (ee != kNoMatch) {
+            if (bb == key[u]) {
+              out = ee;
+              m = 1;
+              break;
+            }
+            ss = (ss + 1) & cmask;
+            ee = tab[ss];
+            if (ee != kNoMatch) bb = bk[ee];
+          }
+          if (WRITE) res[jl] = out;
+          else if (me_out) me_out[jl] = (uint16_t)(out == kNoMatch ? kEmpty16 : out);
+          wcount += m;
+        }
+      }
+    }
+    for (; r < r1; ++r) {
       const uint32_t jl = r * 32 + lane;
       if (jl < nq) {
         const K key = pk[jl];

@@ -483,13 +483,13 @@ __device__ __forceinline__ uint32_t digit_of(K k, const BlockPassArgs& a) {
 // HOT: the pass has one dominant digit `hot` (skewed keys): its lanes take
 // their peer mask from one ballot instead of an atomic OR on a single shared
 // word that a third or more of every warp would hit.
-template <class K, int ITEMS, int RANK, bool SHARD, bool FULL, int RB, bool HOT>
+template <class K, int ITEMS, int RANK, bool SHARD, bool FULL, int RB, bool HOT, int NT>
 __device__ __forceinline__ void scatter_tile(const BlockPassArgs& a, const uint8_t* st,
                                              uint16_t* sidx, uint16_t (*whist)[1 << RB],
                                              uint32_t* mm, uint32_t* dstart, uint32_t* run,
                                              uint32_t* goff, uint32_t* wsum, uint32_t tbase,
                                              uint32_t tile_n, uint32_t hot) {
-  constexpr uint32_t kTile = ITEMS * kTmaThreads;
+  constexpr uint32_t kTile = ITEMS * NT;
   constexpr int kR = 1 << RB;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const K* skey = reinterpret_cast<const K*>(st);
@@ -536,9 +536,9 @@ __device__ __forceinline__ void scatter_tile(const BlockPassArgs& a, const uint8
     // warp's row): the digit scan needs no second barrier
     constexpr int kD = kR / 32, kW = kD / 2;
     if (warp == 0) {
-      uint32_t c[kTmaWarps][kW], r[kD] = {};
+      uint32_t c[(NT / 32)][kW], r[kD] = {};
 #pragma unroll
-      for (int w = 0; w < kTmaWarps; ++w) {
+      for (int w = 0; w < (NT / 32); ++w) {
         const uint32_t* row = reinterpret_cast<const uint32_t*>(&whist[w][0]) + lane * kW;
 #pragma unroll
         for (int j = 0; j < kW; ++j) {
@@ -558,7 +558,7 @@ __device__ __forceinline__ void scatter_tile(const BlockPassArgs& a, const uint8
 #pragma unroll
       for (int j = 0; j < kD; ++j) p[j] = ds[j];
 #pragma unroll
-      for (int w = 0; w < kTmaWarps; ++w) {
+      for (int w = 0; w < (NT / 32); ++w) {
         uint32_t* row = reinterpret_cast<uint32_t*>(&whist[w][0]) + lane * kW;
 #pragma unroll
         for (int j = 0; j < kW; ++j) {
@@ -576,10 +576,10 @@ __device__ __forceinline__ void scatter_tile(const BlockPassArgs& a, const uint8
     }
     __syncthreads();
   } else {
-    uint32_t c[kTmaWarps], r = 0, inc = 0;
+    uint32_t c[(NT / 32)], r = 0, inc = 0;
     if (tid < kR) {
 #pragma unroll
-      for (int w = 0; w < kTmaWarps; ++w) {
+      for (int w = 0; w < (NT / 32); ++w) {
         c[w] = whist[w][tid];
         r += c[w];
       }
@@ -595,7 +595,7 @@ __device__ __forceinline__ void scatter_tile(const BlockPassArgs& a, const uint8
       const uint32_t ds = off + inc - r;
       uint32_t p = ds;
 #pragma unroll
-      for (int w = 0; w < kTmaWarps; ++w) {
+      for (int w = 0; w < (NT / 32); ++w) {
         whist[w][tid] = (uint16_t)p;
         p += c[w];
       }
@@ -621,23 +621,23 @@ __device__ __forceinline__ void scatter_tile(const BlockPassArgs& a, const uint8
   K key[ITEMS];
 #pragma unroll
   for (int k = 0; k < ITEMS; ++k) {
-    const uint32_t j = tid + k * kTmaThreads;
+    const uint32_t j = tid + k * NT;
     src[k] = (FULL || j < tile_n) ? sidx[j] : 0u;
   }
 #pragma unroll
   for (int k = 0; k < ITEMS; ++k) key[k] = skey[src[k]];
 #pragma unroll
-  for (int k = 0; k < ITEMS; ++k) g[k] = goff[digit_of<SHARD>(key[k], a)] + tid + k * kTmaThreads;
+  for (int k = 0; k < ITEMS; ++k) g[k] = goff[digit_of<SHARD>(key[k], a)] + tid + k * NT;
   K* __restrict__ kout = static_cast<K*>(a.keys_out);
 #pragma unroll
   for (int k = 0; k < ITEMS; ++k)
-    if (FULL || tid + k * kTmaThreads < tile_n) kout[g[k]] = key[k];
+    if (FULL || tid + k * NT < tile_n) kout[g[k]] = key[k];
   for (int c = 0; c < a.nvals; ++c) {
     if (a.gen_ids && c == 0) {
       uint32_t* __restrict__ vout = static_cast<uint32_t*>(a.vout[c]);
 #pragma unroll
       for (int k = 0; k < ITEMS; ++k)
-        if (FULL || tid + k * kTmaThreads < tile_n) vout[g[k]] = tbase + src[k];
+        if (FULL || tid + k * NT < tile_n) vout[g[k]] = tbase + src[k];
     } else if (a.vbytes[c] == 4) {
       const uint32_t* sv = reinterpret_cast<const uint32_t*>(st + a.voff[c]);
       uint32_t* __restrict__ vout = static_cast<uint32_t*>(a.vout[c]);
@@ -646,7 +646,7 @@ __device__ __forceinline__ void scatter_tile(const BlockPassArgs& a, const uint8
       for (int k = 0; k < ITEMS; ++k) v[k] = sv[src[k]];
 #pragma unroll
       for (int k = 0; k < ITEMS; ++k)
-        if (FULL || tid + k * kTmaThreads < tile_n) vout[g[k]] = v[k];
+        if (FULL || tid + k * NT < tile_n) vout[g[k]] = v[k];
     } else {
       const uint64_t* sv = reinterpret_cast<const uint64_t*>(st + a.voff[c]);
       uint64_t* __restrict__ vout = static_cast<uint64_t*>(a.vout[c]);
@@ -655,17 +655,17 @@ __device__ __forceinline__ void scatter_tile(const BlockPassArgs& a, const uint8
       for (int k = 0; k < ITEMS; ++k) v[k] = sv[src[k]];
 #pragma unroll
       for (int k = 0; k < ITEMS; ++k)
-        if (FULL || tid + k * kTmaThreads < tile_n) vout[g[k]] = v[k];
+        if (FULL || tid + k * NT < tile_n) vout[g[k]] = v[k];
     }
   }
   CJ_CLK(7);
   (void)kTile;
 }
 
-template <class K, int ITEMS, int RANK, bool SHARD, int MINB, int RB>
-__global__ void __launch_bounds__(kTmaThreads, MINB)
+template <class K, int ITEMS, int RANK, bool SHARD, int MINB, int RB, int NT>
+__global__ void __launch_bounds__(NT, MINB)
 k_scatter_v2(const __grid_constant__ BlockPassArgs a) {
-  constexpr uint32_t kTile = ITEMS * kTmaThreads;
+  constexpr uint32_t kTile = ITEMS * NT;
   constexpr int kR = 1 << RB;
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* const stage0 = smem;
@@ -673,7 +673,7 @@ k_scatter_v2(const __grid_constant__ BlockPassArgs a) {
   // per-warp peer masks (rank mode 0) after the source indices, 16-byte aligned
   uint32_t (*match_word)[kR] = reinterpret_cast<uint32_t (*)[kR]>(
       smem + (((size_t)a.stages * a.stage_bytes + (size_t)kTile * 2 + 15) & ~size_t(15)));
-  __shared__ uint16_t whist[kTmaWarps][kR];
+  __shared__ uint16_t whist[(NT / 32)][kR];
   __shared__ uint32_t dstart[kR];
   __shared__ uint32_t run[kR];   // next global row of each digit in this block
   __shared__ uint32_t goff[kR];  // global row of tile slot 0 of each digit's run (mod 2^32)
@@ -707,7 +707,7 @@ k_scatter_v2(const __grid_constant__ BlockPassArgs a) {
     if (t_begin < t_end && full_tile(t_begin)) issue(0, t_begin);
   }
   if (RANK == 0)
-    for (int i = tid; i < kTmaWarps * kR; i += kTmaThreads) (&match_word[0][0])[i] = 0;
+    for (int i = tid; i < (NT / 32) * kR; i += NT) (&match_word[0][0])[i] = 0;
   __shared__ uint64_t s_dmax[kR / 32];
   if (tid < kR) {
     uint64_t c = a.base[tid];
@@ -751,28 +751,28 @@ k_scatter_v2(const __grid_constant__ BlockPassArgs a) {
       dev::mbar_wait(&mbar[b], b ? ph1 : ph0);
       if (b) ph1 ^= 1; else ph0 ^= 1;
       if (hot != 0xffffffffu)
-        scatter_tile<K, ITEMS, RANK, SHARD, true, RB, true>(a, st, sidx, whist, mm, dstart, run, goff,
+        scatter_tile<K, ITEMS, RANK, SHARD, true, RB, true, NT>(a, st, sidx, whist, mm, dstart, run, goff,
                                                             wsum, (uint32_t)tbase, tile_n, hot);
       else
-        scatter_tile<K, ITEMS, RANK, SHARD, true, RB, false>(a, st, sidx, whist, mm, dstart, run, goff,
+        scatter_tile<K, ITEMS, RANK, SHARD, true, RB, false, NT>(a, st, sidx, whist, mm, dstart, run, goff,
                                                              wsum, (uint32_t)tbase, tile_n, hot);
     } else {  // last, partial tile: plain loads
       K* wk = reinterpret_cast<K*>(st);
-      for (uint32_t j = tid; j < kTile; j += kTmaThreads) wk[j] = j < tile_n ? kin[tbase + j] : K(0);
+      for (uint32_t j = tid; j < kTile; j += NT) wk[j] = j < tile_n ? kin[tbase + j] : K(0);
       for (int c = 0; c < a.nvals; ++c) {
         if (a.gen_ids && c == 0) continue;
         if (a.vbytes[c] == 4) {
           const uint32_t* src = static_cast<const uint32_t*>(a.vin[c]) + tbase;
           uint32_t* dst = reinterpret_cast<uint32_t*>(st + a.voff[c]);
-          for (uint32_t j = tid; j < tile_n; j += kTmaThreads) dst[j] = src[j];
+          for (uint32_t j = tid; j < tile_n; j += NT) dst[j] = src[j];
         } else {
           const uint64_t* src = static_cast<const uint64_t*>(a.vin[c]) + tbase;
           uint64_t* dst = reinterpret_cast<uint64_t*>(st + a.voff[c]);
-          for (uint32_t j = tid; j < tile_n; j += kTmaThreads) dst[j] = src[j];
+          for (uint32_t j = tid; j < tile_n; j += NT) dst[j] = src[j];
         }
       }
       __syncthreads();
-      scatter_tile<K, ITEMS, RANK, SHARD, false, RB, false>(a, st, sidx, whist, mm, dstart, run, goff,
+      scatter_tile<K, ITEMS, RANK, SHARD, false, RB, false, NT>(a, st, sidx, whist, mm, dstart, run, goff,
                                                             wsum, (uint32_t)tbase, tile_n, hot);
     }
     __syncthreads();
@@ -784,39 +784,47 @@ k_scatter_v2(const __grid_constant__ BlockPassArgs a) {
 }
 
 template <class K, int ITEMS, int RANK, int MINB, int RB>
-void launch_v2(cj_ctx* ctx, const BlockPassArgs& a, size_t smem) {
-  auto kern = a.hparts ? k_scatter_v2<K, ITEMS, RANK, true, MINB, RB>
-                       : k_scatter_v2<K, ITEMS, RANK, false, MINB, RB>;
-  CJ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<a.nblocks, kTmaThreads, smem, ctx->stream>>>(a);
+void launch_v2(cj_ctx* ctx, const BlockPassArgs& a, size_t smem, int threads) {
+  auto go = [&](auto kern, int nt) {
+    CJ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<a.nblocks, nt, smem, ctx->stream>>>(a);
+  };
+  if (threads == 256) {  // two CTAs per SM
+    if (a.hparts) go(k_scatter_v2<K, ITEMS, RANK, true, 2, RB, 256>, 256);
+    else go(k_scatter_v2<K, ITEMS, RANK, false, 2, RB, 256>, 256);
+  } else {
+    if (a.hparts) go(k_scatter_v2<K, ITEMS, RANK, true, MINB, RB, 512>, 512);
+    else go(k_scatter_v2<K, ITEMS, RANK, false, MINB, RB, 512>, 512);
+  }
 }
 
 template <class K, int RANK>
-void launch_v2_items(cj_ctx* ctx, const BlockPassArgs& a, size_t smem, int items, int rb) {
+void launch_v2_items(cj_ctx* ctx, const BlockPassArgs& a, size_t smem, int items, int rb,
+                     int threads) {
   if (rb == 6) {  // passes of <= 6 bits: 64-digit tables, room for 8192-row tiles
     switch (items) {
-      case 16: launch_v2<K, 16, RANK, 1, 6>(ctx, a, smem); break;
-      case 12: launch_v2<K, 12, RANK, 1, 6>(ctx, a, smem); break;
-      case 8: launch_v2<K, 8, RANK, 1, 6>(ctx, a, smem); break;
-      default: launch_v2<K, 4, RANK, 1, 6>(ctx, a, smem); break;
+      case 16: launch_v2<K, 16, RANK, 1, 6>(ctx, a, smem, threads); break;
+      case 12: launch_v2<K, 12, RANK, 1, 6>(ctx, a, smem, threads); break;
+      case 8: launch_v2<K, 8, RANK, 1, 6>(ctx, a, smem, threads); break;
+      default: launch_v2<K, 4, RANK, 1, 6>(ctx, a, smem, threads); break;
     }
     return;
   }
   if (rb == 7) {  // 7-bit passes (27-bit sort keys: 7+7+7+6)
     switch (items) {
-      case 16: launch_v2<K, 16, RANK, 1, 7>(ctx, a, smem); break;
-      case 12: launch_v2<K, 12, RANK, 1, 7>(ctx, a, smem); break;
-      case 8: launch_v2<K, 8, RANK, 1, 7>(ctx, a, smem); break;
-      default: launch_v2<K, 4, RANK, 1, 7>(ctx, a, smem); break;
+      case 16: launch_v2<K, 16, RANK, 1, 7>(ctx, a, smem, threads); break;
+      case 12: launch_v2<K, 12, RANK, 1, 7>(ctx, a, smem, threads); break;
+      case 8: launch_v2<K, 8, RANK, 1, 7>(ctx, a, smem, threads); break;
+      default: launch_v2<K, 4, RANK, 1, 7>(ctx, a, smem, threads); break;
     }
     return;
   }
   if (rb != 8) fail(CJ_ERR_UNSUPPORTED, "scatter pass digits wider than 8 bits");
   switch (items) {
-    case 16: launch_v2<K, 16, RANK, 1, 8>(ctx, a, smem); break;
-    case 12: launch_v2<K, 12, RANK, 1, 8>(ctx, a, smem); break;
-    case 8: launch_v2<K, 8, RANK, 1, 8>(ctx, a, smem); break;
-    default: launch_v2<K, 4, RANK, 1, 8>(ctx, a, smem); break;
+    case 16: launch_v2<K, 16, RANK, 1, 8>(ctx, a, smem, threads); break;
+    case 12: launch_v2<K, 12, RANK, 1, 8>(ctx, a, smem, threads); break;
+    case 8: launch_v2<K, 8, RANK, 1, 8>(ctx, a, smem, threads); break;
+    default: launch_v2<K, 4, RANK, 1, 8>(ctx, a, smem, threads); break;
   }
 }
 
@@ -858,19 +866,23 @@ ScatterGeom scatter_geom(cj_ctx* ctx, uint64_t n, int key_bytes, const ValCols& 
   const char* e_stages = std::getenv("CJ_SCATTER_STAGES");
   const char* e_rank = std::getenv("CJ_RANK");
   g.rank = e_rank ? std::atoi(e_rank) : 0;
-  g.ctas_per_sm = 1;  // (2 CTAs/SM with single stages measured slower: profiles/)
+  // CJ_SCATTER_THREADS=256: two 256-thread CTAs per SM, each with half the
+  // shared memory (experiment knob; default one 512-thread CTA per SM)
+  const char* e_thr = std::getenv("CJ_SCATTER_THREADS");
+  g.threads = e_thr && std::atoi(e_thr) == 256 ? 256 : 512;
+  g.ctas_per_sm = g.threads == 256 ? 2 : 1;
   g.stages = e_stages ? std::min(2, std::max(1, std::atoi(e_stages))) : 2;
   const int want_items = e_items ? std::atoi(e_items) : 16;
   // 227 KB per CTA minus the static arrays (per-warp digit counts 8 KB and
   // ~4 KB of cursors, twice that for 9-bit digits) and the dynamic peer masks
   // of rank mode 0 (16 KB / 32 KB)
-  const size_t budget = (227 - (((size_t)12 << rb) >> 8)) * 1024;
-  const size_t match = g.rank == 0 ? (size_t)kTmaWarps * 4 << rb : 0;
+  const size_t budget = (227 / g.ctas_per_sm - (((size_t)12 << rb) >> 8)) * 1024;
+  const size_t match = g.rank == 0 ? (size_t)(g.threads / 32) * 4 << rb : 0;
   for (int items : {16, 12, 8, 4}) {
     if (items > want_items && items > 4) continue;
     if (rb == 9 && items > 12) continue;
     g.items = items;
-    g.tile = (uint64_t)kTmaThreads * items;
+    g.tile = (uint64_t)g.threads * items;
     g.stage_bytes = (uint32_t)(g.tile * row);
     g.pbytes = 0;
     g.smem = (((size_t)g.stages * g.stage_bytes + g.tile * 2 + 15) & ~size_t(15)) + match;
@@ -988,11 +1000,11 @@ void scatter_pass(cj_ctx* ctx, const void* keys_in, void* keys_out, uint64_t n, 
     }
     ctx->kbegin("scatter_pass", n * (row + wrow));
     if (key_bytes == 4) {
-      if (g.rank == 1) launch_v2_items<uint32_t, 1>(ctx, a, g.smem, g.items, g.rb);
-      else launch_v2_items<uint32_t, 0>(ctx, a, g.smem, g.items, g.rb);
+      if (g.rank == 1) launch_v2_items<uint32_t, 1>(ctx, a, g.smem, g.items, g.rb, g.threads);
+      else launch_v2_items<uint32_t, 0>(ctx, a, g.smem, g.items, g.rb, g.threads);
     } else {
-      if (g.rank == 1) launch_v2_items<uint64_t, 1>(ctx, a, g.smem, g.items, g.rb);
-      else launch_v2_items<uint64_t, 0>(ctx, a, g.smem, g.items, g.rb);
+      if (g.rank == 1) launch_v2_items<uint64_t, 1>(ctx, a, g.smem, g.items, g.rb, g.threads);
+      else launch_v2_items<uint64_t, 0>(ctx, a, g.smem, g.items, g.rb, g.threads);
     }
     ctx->kend();
     CJ_CUDA(cudaGetLastError());

@@ -1,11 +1,8 @@
 cd $GRAFT_REPO_ROOT 2>/dev/null || cd /root/repo
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q > gpurun_out/t_parity.log 2>&1; echo "exit $?" >> gpurun_out/t_parity.log
-tail -5 gpurun_out/t_parity.log
-for env in "CJ_RANK=1" "CJ_RANK=0" "CJ_SCATTER_WARP=0"; do
-  echo "== $env" >> gpurun_out/diag.log
-  env $env timeout 300 python tools/diag.py phj-gftr smj-gftr phj-gfur >> gpurun_out/diag.log 2>&1
-done
-tail -60 gpurun_out/diag.log
-timeout 300 python bench.py --config C3 --no-extras --steps 3 --warmup 2 > gpurun_out/c3.json 2>&1
-head -c 700 gpurun_out/c3.json
+timeout 2400 python -m pytest tests/test_gpu_shard.py tests/test_gpu_scale.py -x -q > gpurun_out/t_shard.log 2>&1; echo "exit $?" >> gpurun_out/t_shard.log
+tail -15 gpurun_out/t_shard.log
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 1 --sharded --steps 5 --warmup 3 --no-extras > gpurun_out/sharded.json 2> gpurun_out/sharded.err
+python -c "
+import json; d=json.loads(open('gpurun_out/sharded.json').read().strip().splitlines()[-1]); print(d['ms_per_step'], d['phases_ms'], d['shuffle']); [print(k) for k in d['kernels'][:6]]"
+tail -3 gpurun_out/sharded.err
