@@ -198,9 +198,16 @@ typedef struct {
   uint64_t transform_ns, find_ns, materialize_ns;   /* PhaseReport (mem_ledger.hpp:231-246) */
   double clusteredness_r, clusteredness_s;          /* JoinStats (join_engine.hpp:54-58) */
   uint64_t device_bytes_peak;      /* scratch + outputs held by the call */
-  /* PhaseReport::peak_by_phase (mem_ledger.hpp:231-246): device bytes the call
-   * held at its high-water mark in each phase */
+  /* device bytes the call held (outputs included) at its high-water mark in
+   * each phase */
   uint64_t peak_transform_b, peak_find_b, peak_materialize_b;
+  /* PhaseReport::peak_by_phase (mem_ledger.hpp:26-100, 231-246): per phase
+   * [transform, find, materialize], at the high-water mark of their sum, the
+   * logical bytes of column-sized working data (transformed keys and carried
+   * columns, tuple-id maps) and of scratch (LSD ping-pong, histograms,
+   * layouts, find scratch); the output relation is not counted */
+  uint64_t ledger_column_b[3];
+  uint64_t ledger_scratch_b[3];
 } cj_join_result;
 
 void cj_default_options(cj_join_options* opt);

@@ -73,7 +73,8 @@ class JoinResult(C.Structure):
                 ("find_ns", C.c_uint64), ("materialize_ns", C.c_uint64),
                 ("clusteredness_r", C.c_double), ("clusteredness_s", C.c_double),
                 ("device_bytes_peak", C.c_uint64), ("peak_transform_b", C.c_uint64),
-                ("peak_find_b", C.c_uint64), ("peak_materialize_b", C.c_uint64)]
+                ("peak_find_b", C.c_uint64), ("peak_materialize_b", C.c_uint64),
+                ("ledger_column_b", C.c_uint64 * 3), ("ledger_scratch_b", C.c_uint64 * 3)]
 
 
 class SequenceStep(C.Structure):

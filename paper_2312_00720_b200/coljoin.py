@@ -298,6 +298,10 @@ class PhaseReport:
     find_ns: int = 0
     materialize_ns: int = 0
     peak_by_phase: tuple = (0, 0, 0)
+    # MemLedger view (mem_ledger.hpp:26-100) per phase: logical bytes of
+    # column-sized working data and of scratch at the phase's high-water mark
+    column_bytes: tuple = (0, 0, 0)
+    scratch_bytes: tuple = (0, 0, 0)
 
     def total_ns(self) -> int:
         return self.transform_ns + self.find_ns + self.materialize_ns
@@ -367,7 +371,8 @@ def join_output(ctx: Context, res, R, S, build: Relation, probe: Relation, kw) -
     rel = Relation(key, pays, name=(build.name + "_" + probe.name) or "join")
     return JoinOutput(rel, PhaseReport(res.transform_ns, res.find_ns, res.materialize_ns,
                                        (res.peak_transform_b, res.peak_find_b,
-                                        res.peak_materialize_b)), t,
+                                        res.peak_materialize_b),
+                                       tuple(res.ledger_column_b), tuple(res.ledger_scratch_b)), t,
                       res.clusteredness_r if kw.get("want_stats") else 1.0,
                       res.clusteredness_s if kw.get("want_stats") else 1.0, ids_r, ids_s)
 
@@ -435,7 +440,8 @@ def run_join_host(ctx: Context, build: Relation, probe: Relation, algo="phj", pa
     ids_s = arena.take(res.ids_s, t, 4) if res.ids_s else None
     out = JoinOutput(Relation(key, pays),
                      PhaseReport(res.transform_ns, res.find_ns, res.materialize_ns,
-                                 (res.peak_transform_b, res.peak_find_b, res.peak_materialize_b)),
+                                 (res.peak_transform_b, res.peak_find_b, res.peak_materialize_b),
+                                 tuple(res.ledger_column_b), tuple(res.ledger_scratch_b)),
                      t,
                      res.clusteredness_r, res.clusteredness_s, ids_r, ids_s)
     return out, h2d.value, d2h.value

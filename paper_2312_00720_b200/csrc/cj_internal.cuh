@@ -39,9 +39,18 @@ struct cj_ctx {
   uint16_t epoch = 0;             // look-back status generation (see radix.cu)
   uint64_t launches = 0;          // kernels launched through this ctx
   uint64_t scratch_now = 0, scratch_peak = 0;  // device scratch held by operators
-  // every live alloc() of this ctx (bytes), for run_join's per-phase peaks
-  std::unordered_map<void*, uint64_t> live_sizes;
+  // every live alloc() of this ctx, for run_join's per-phase peaks: device
+  // bytes, and the MemLedger view (mem_ledger.hpp:26-100) — the logical bytes
+  // of column-sized working data vs scratch; the output relation is neither
+  enum : int { kScratchData = 0, kColumnData = 1, kOutputData = 2 };
+  struct LiveAlloc {
+    uint64_t bytes, logical;
+    int cls;
+  };
+  std::unordered_map<void*, LiveAlloc> live_sizes;
   uint64_t live = 0, live_peak = 0;
+  uint64_t ledger[2] = {0, 0};        // live logical scratch / column bytes
+  uint64_t ledger_peak[2] = {0, 0};   // both, at the high-water mark of their sum
   std::string last_error;
   // persistent scratch (grown on demand, never shrunk)
   uint64_t* status = nullptr;     // decoupled look-back words
@@ -66,7 +75,13 @@ struct cj_ctx {
   void kend();                                       // after it
   void set_bytes(const char* name, uint64_t bytes);  // fix up the last record of `name`
 
-  void* alloc(uint64_t bytes);
+  // cls: kScratchData / kColumnData / kOutputData; logical = the bytes the
+  // ledger counts (default `bytes`; padded columns pass their unpadded size)
+  void* alloc(uint64_t bytes, int cls = kScratchData, uint64_t logical = ~0ull);
+  void ledger_reset_peak() {
+    ledger_peak[0] = ledger[0];
+    ledger_peak[1] = ledger[1];
+  }
   void release(void* p);
   uint16_t next_epoch();          // fresh look-back generation (memsets on wrap)
   uint64_t* status_buffer(uint64_t words);

@@ -240,7 +240,7 @@ Side transform(cj_ctx* ctx, const cj_relation* rel, int algo, bool gfur, unsigne
   Side s;
   const uint64_t n = rel->rows;
   const int kb = (int)rel->key_bytes;
-  s.keys = ctx->alloc(n * kb + kPad);
+  s.keys = ctx->alloc(n * kb + kPad, cj_ctx::kColumnData, n * kb);
   owned.push_back(s.keys);
   ValCols v;
   if (gfur) {
@@ -248,14 +248,15 @@ Side transform(cj_ctx* ctx, const cj_relation* rel, int algo, bool gfur, unsigne
     v.gen_ids = 1;
     v.in[0] = nullptr;
     v.bytes[0] = 4;
-    v.out[0] = ctx->alloc(n * 4 + kPad);
+    v.out[0] = ctx->alloc(n * 4 + kPad, cj_ctx::kColumnData, n * 4);
     owned.push_back(v.out[0]);
   } else {
     v.n = (int)rel->npay;
     for (uint32_t c = 0; c < rel->npay; ++c) {
       v.in[c] = rel->pay[c];
       v.bytes[c] = rel->pay_bytes[c];
-      v.out[c] = ctx->alloc(n * rel->pay_bytes[c] + kPad);
+      v.out[c] = ctx->alloc(n * rel->pay_bytes[c] + kPad, cj_ctx::kColumnData,
+                            n * rel->pay_bytes[c]);
       owned.push_back(v.out[c]);
     }
   }
@@ -292,12 +293,14 @@ Side transform(cj_ctx* ctx, const cj_relation* rel, int algo, bool gfur, unsigne
 void alloc_output(cj_ctx* ctx, const cj_relation* r, const cj_relation* s, uint64_t cap,
                   bool ids, cj_join_result* res) {
   const uint64_t c = std::max<uint64_t>(cap, 1);
-  res->key = ctx->alloc(c * r->key_bytes);
-  for (uint32_t i = 0; i < r->npay; ++i) res->pay[i] = ctx->alloc(c * r->pay_bytes[i]);
-  for (uint32_t i = 0; i < s->npay; ++i) res->pay[r->npay + i] = ctx->alloc(c * s->pay_bytes[i]);
-  if (ids) {
-    res->ids_r = static_cast<uint32_t*>(ctx->alloc(c * 4));
-    res->ids_s = static_cast<uint32_t*>(ctx->alloc(c * 4));
+  constexpr int kOut = cj_ctx::kOutputData, kCol = cj_ctx::kColumnData;
+  res->key = ctx->alloc(c * r->key_bytes, kOut);
+  for (uint32_t i = 0; i < r->npay; ++i) res->pay[i] = ctx->alloc(c * r->pay_bytes[i], kOut);
+  for (uint32_t i = 0; i < s->npay; ++i)
+    res->pay[r->npay + i] = ctx->alloc(c * s->pay_bytes[i], kOut);
+  if (ids) {  // the tuple-id maps: column data (join_engine.cpp:300-301), |T| entries
+    res->ids_r = static_cast<uint32_t*>(ctx->alloc(c * 4, kCol, cap * 4));
+    res->ids_s = static_cast<uint32_t*>(ctx->alloc(c * 4, kCol, cap * 4));
   }
 }
 
@@ -316,13 +319,32 @@ void free_output(cj_ctx* ctx, cj_join_result* res) {
 // Device bytes this call holds (outputs, transformed columns, scratch) at
 // their high-water mark in each phase — PhaseReport's per-phase peaks
 // (mem_ledger.hpp:231-246) measured on the device arena instead of a ledger.
+// The ledger view follows MemLedger::begin_phase (mem_ledger.hpp:40-47): bytes
+// carried in from earlier phases count toward a phase's peak; each phase's
+// snapshot is (column, scratch) at the high-water mark of their sum.
 struct PhasePeaks {
   cj_ctx* ctx;
   uint64_t base;
-  explicit PhasePeaks(cj_ctx* c) : ctx(c), base(c->live) { c->live_peak = c->live; }
+  uint64_t lbase[2];
+  int phase = 0;
+  cj_join_result* res;
+  PhasePeaks(cj_ctx* c, cj_join_result* r) : ctx(c), base(c->live), res(r) {
+    c->live_peak = c->live;
+    lbase[0] = c->ledger[0];
+    lbase[1] = c->ledger[1];
+    c->ledger_reset_peak();
+  }
   uint64_t next() {  // peak since the last call; starts the next phase
     const uint64_t p = ctx->live_peak > base ? ctx->live_peak - base : 0;
     ctx->live_peak = ctx->live;
+    if (phase < 3) {
+      res->ledger_column_b[phase] =
+          ctx->ledger_peak[1] > lbase[1] ? ctx->ledger_peak[1] - lbase[1] : 0;
+      res->ledger_scratch_b[phase] =
+          ctx->ledger_peak[0] > lbase[0] ? ctx->ledger_peak[0] - lbase[0] : 0;
+    }
+    ++phase;
+    ctx->ledger_reset_peak();
     return p;
   }
 };
@@ -365,7 +387,7 @@ void run_join_dev(cj_ctx* ctx, const cj_relation* R, const cj_relation* S,
     }
   } guard{ctx, &owned};
 
-  PhasePeaks peaks(ctx);
+  PhasePeaks peaks(ctx, res);
   if (opt->algo == CJ_NPHJ) {
     // No transform: the build relation is hashed as is (nphj.cu).
     if (hooks && hooks->before_side) {
@@ -541,6 +563,12 @@ void run_join_dev(cj_ctx* ctx, const cj_relation* R, const cj_relation* S,
     const uint64_t b = rrow * R->rows + srow * S->rows + out_row * total;
     ctx->set_bytes(opt->algo == CJ_SMJ ? "smj_find" : "phj_find", b);
   }
+  // the transformed sides are done with (GFTR's find wrote finished rows;
+  // GFUR gathers from the untransformed relations): released at the end of
+  // the find phase, as join_engine.cpp:330-335 frees the transformed keys and
+  // ids
+  for (void* p : owned) ctx->release(p);
+  owned.clear();
   tm.mark(2);
   res->peak_find_b = peaks.next();
 
@@ -563,7 +591,6 @@ void run_join_dev(cj_ctx* ctx, const cj_relation* R, const cj_relation* S,
     gather_cols(ctx, in, S->rows, res->ids_s, total, out, by, (int)S->npay);
   }
   tm.mark(3);
-  // the transformed columns are still held here (released with `owned`)
   res->peak_materialize_b = peaks.next();
   res->device_bytes_peak =
       std::max({res->peak_transform_b, res->peak_find_b, res->peak_materialize_b});
@@ -588,12 +615,17 @@ void run_join_dev(cj_ctx* ctx, const cj_relation* R, const cj_relation* S,
 
 // ---- cj_ctx -------------------------------------------------------------------
 
-void* cj_ctx::alloc(uint64_t bytes) {
+void* cj_ctx::alloc(uint64_t bytes, int cls, uint64_t logical) {
   void* p = nullptr;
   cj::check_cuda(cudaMallocFromPoolAsync(&p, bytes ? bytes : 16, pool, stream), "cudaMallocAsync");
-  live_sizes[p] = bytes;
+  if (logical == ~0ull) logical = bytes;
+  live_sizes[p] = LiveAlloc{bytes, logical, cls};
   live += bytes;
   live_peak = std::max(live_peak, live);
+  if (cls != kOutputData) {
+    ledger[cls] += logical;
+    if (ledger[0] + ledger[1] > ledger_peak[0] + ledger_peak[1]) ledger_reset_peak();
+  }
   return p;
 }
 
@@ -601,7 +633,8 @@ void cj_ctx::release(void* p) {
   if (!p) return;
   auto it = live_sizes.find(p);
   if (it != live_sizes.end()) {
-    live -= it->second;
+    live -= it->second.bytes;
+    if (it->second.cls != kOutputData) ledger[it->second.cls] -= it->second.logical;
     live_sizes.erase(it);
   }
   cudaFreeAsync(p, stream);

@@ -739,9 +739,12 @@ JoinOutput run_join(const JoinTask& task) {
   out.report.transform_ns = res.transform_ns;
   out.report.find_ns = res.find_ns;
   out.report.materialize_ns = res.materialize_ns;
-  out.report.peak_by_phase[0].total_bytes = res.peak_transform_b;
-  out.report.peak_by_phase[1].total_bytes = res.peak_find_b;
-  out.report.peak_by_phase[2].total_bytes = res.peak_materialize_b;
+  // MemLedger view (mem_ledger.hpp:26-100): column data + scratch per phase
+  for (int ph = 0; ph < 3; ++ph) {
+    out.report.peak_by_phase[ph].column_bytes = res.ledger_column_b[ph];
+    out.report.peak_by_phase[ph].scratch_bytes = res.ledger_scratch_b[ph];
+    out.report.peak_by_phase[ph].total_bytes = res.ledger_column_b[ph] + res.ledger_scratch_b[ph];
+  }
   out.stats.matches = res.rows;
   out.stats.clusteredness_r = res.clusteredness_r;
   out.stats.clusteredness_s = res.clusteredness_s;

@@ -422,3 +422,44 @@ def test_smj_mislabelled_unique_build(ctx, kb):
     rk = g.integers(0, n, n, dtype=np.uint64).astype(dt)
     sk = g.permutation(n).astype(dt)
     _smj_case(ctx, rk, sk, True, seed=kb)
+
+
+# ---- MemLedger view of the device arena (mem_ledger.hpp:26-100) --------------
+def dev_rel(X, uniq):
+    return cj.Relation(cj.to_device(X["key"]), [cj.to_device(p) for p in X["payloads"]], "",
+                       uniq)
+
+
+# |R| = |S| = |T| = n at full match, 4-byte key + one 4-byte payload per side,
+# M_c = 4n (one column).  This engine's closed forms:
+#   GFUR: transform 4 M_c (keys + ids per side; the ids are born in the first
+#         scatter pass, no iota column: the reference's 5th M_c),
+#         find 6 M_c (+ the two id maps), materialise 2 M_c (the id maps);
+#   GFTR: transform 4 M_c, find 4 M_c + 2 M_c when id maps are requested (the
+#         fused find writes finished rows), materialise: the id maps only
+#         (the transformed payloads were consumed by the fused find; the
+#         reference's 4 M_c holds them until its gather).
+@pytest.mark.parametrize("algo", ["phj", "smj"])
+@pytest.mark.parametrize("rows", [4096, 65536])
+def test_ledger_closed_forms(ctx, algo, rows):
+    R, S = O.gen_pk_fk(rows, rows, 1, 1, seed=77)
+    Rd, Sd = dev_rel(R, True), dev_rel(S, False)
+    mc = rows * 4
+    gfur = cj.run_join(ctx, Rd, Sd, algo, "gfur", want_ids=True).report
+    assert gfur.column_bytes == (4 * mc, 6 * mc, 2 * mc)
+    assert gfur.scratch_bytes[0] > 0
+    gftr = cj.run_join(ctx, Rd, Sd, algo, "gftr", want_ids=True).report
+    assert gftr.column_bytes == (4 * mc, 6 * mc, 2 * mc)
+    plain = cj.run_join(ctx, Rd, Sd, algo, "gftr").report
+    assert plain.column_bytes == (4 * mc, 4 * mc, 0)
+    total = lambda r: max(c + s for c, s in zip(r.column_bytes, r.scratch_bytes))  # noqa: E731
+    assert total(gftr) <= total(gfur)
+    assert total(plain) <= total(gfur)
+
+
+def test_ledger_zero_rows(ctx):
+    e = np.zeros(0, np.uint32)
+    Rd = cj.Relation(cj.to_device(e), [cj.to_device(e)], "R", True)
+    Sd = cj.Relation(cj.to_device(e), [cj.to_device(e)], "S", False)
+    out = cj.run_join(ctx, Rd, Sd, "phj", "gftr")
+    assert out.report.column_bytes[0] == 0 and out.report.column_bytes[2] == 0

@@ -12,7 +12,14 @@ from paper_2312_00720_b200 import _capi as A  # noqa: E402
 ctx = cj.Context(0)
 L = A.lib()
 nr, ns = (1 << 27) >> int(os.environ.get("SCALE", "0")), (1 << 28) >> int(os.environ.get("SCALE", "0"))
-R, S = cj.gen_pk_fk(ctx, nr, ns, 2, 2, 4, 4, 1.0, 0.0, 42)
+# CONFIG=C3|C4z0.5|C4z1.0|C4z1.5|C1 picks a bench.py CONFIGS workload (default C2)
+if os.environ.get("CONFIG"):
+    import bench
+    cfg = bench.CONFIGS[os.environ["CONFIG"]]
+    nr, ns = cfg["r"], cfg["s"]
+    R, S = bench.gen_config(ctx, cfg, nr, ns)
+else:
+    R, S = cj.gen_pk_fk(ctx, nr, ns, 2, 2, 4, 4, 1.0, 0.0, 42)
 Rc, Sc = cj.coljoin.c_relation(R), cj.coljoin.c_relation(S)
 for variant in sys.argv[1:] or ["phj-gftr", "smj-gftr"]:
     opt = cj.options(*variant.split("-"))
@@ -33,6 +40,9 @@ for variant in sys.argv[1:] or ["phj-gftr", "smj-gftr"]:
         per = {}
         for i in range(cnt.value):
             per[names[i].decode()] = per.get(names[i].decode(), 0) + kms[i]
+        if os.environ.get("PERLAUNCH") and it == 3:
+            for i in range(cnt.value):
+                print(f"   {names[i].decode():14s} {kms[i]:.3f} ms  {kby[i] / 1e9:.2f} GB")
         print(variant, it, f"wall={1e3*(t1-t0):.2f} event={e0.elapsed_time(e1):.2f} "
               f"phases={res.transform_ns/1e6:.2f}/{res.find_ns/1e6:.2f}/{res.materialize_ns/1e6:.2f} "
               f"kernels={ksum:.2f} n={cnt.value} rows={res.rows}",
