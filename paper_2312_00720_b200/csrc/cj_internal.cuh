@@ -154,7 +154,7 @@ ScatterGeom scatter_geom(cj_ctx* ctx, uint64_t n, int key_bytes, const ValCols& 
 // read of the keys, over the blocks of geometry g.
 void block_hist(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes, const PassPlan& plan,
                 const ScatterGeom& g, uint32_t* cnt_dev, uint32_t hparts = 0,
-                uint32_t lowbits = 0);
+                uint32_t lowbits = 0, unsigned long long* key_or = nullptr);
 
 // block_hist + digit totals (totals_dev[p*256+d]) + exclusive digit bases
 // (base_dev[p*256+d]); totals_host after one host round trip when non-null.
@@ -162,7 +162,7 @@ void histogram_passes(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes,
                       const PassPlan& plan, const ScatterGeom& g, uint32_t* cnt_dev,
                       uint32_t* totals_dev, uint64_t* base_dev,
                       std::vector<uint32_t>* totals_host, uint32_t hparts = 0,
-                      uint32_t lowbits = 0);
+                      uint32_t lowbits = 0, unsigned long long* key_or = nullptr);
 
 // One stable scatter pass.  With per-block counts of this pass (cnt, stride
 // cnt_stride) and a TMA-eligible geometry it runs the blocked kernel (no
@@ -183,7 +183,8 @@ void shard_partition(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, 
 // pass lands in the caller's outputs.  gen_ids handled in the first pass.
 void lsd_partition(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, int key_bytes,
                    const PassPlan& plan, const ValCols& vals,
-                   std::vector<uint32_t>* counts_host = nullptr);
+                   std::vector<uint32_t>* counts_host = nullptr,
+                   unsigned long long* key_or = nullptr);
 
 // Layout offsets (fanout + 1) of keys sorted by their low `bits`: binary search
 // of every boundary.
@@ -226,12 +227,16 @@ constexpr uint64_t kPad = 64;
 // hash_join.cu: partitioned hash join (count + look-back + fill), outputs per
 // OutSpec; capacity = rows the outputs can hold (CJ_ERR_CAPACITY_EXCEEDED
 // beyond).  Returns the match count (one host sync).
+// key_or (optional, device): OR of the build keys; when (OR >> log2 fanout)
+// is below a unit's table size the unit uses a direct-addressed table.
 uint64_t phj_find(cj_ctx* ctx, const void* bkeys, const uint64_t* boff, const void* pkeys,
                   const uint64_t* poff, uint32_t fanout, int key_bytes, uint32_t limit,
-                  const OutSpec& out, uint64_t capacity);
+                  const OutSpec& out, uint64_t capacity,
+                  const unsigned long long* key_or = nullptr);
 // Match count only (for sizing outputs), plus optional per-reference-unit counts.
 uint64_t phj_count(cj_ctx* ctx, const void* bkeys, const uint64_t* boff, const void* pkeys,
-                   const uint64_t* poff, uint32_t fanout, int key_bytes, uint32_t limit);
+                   const uint64_t* poff, uint32_t fanout, int key_bytes, uint32_t limit,
+                   const unsigned long long* key_or = nullptr);
 
 // merge_join.cu: merge join over sorted keys; same contract.
 uint64_t smj_find(cj_ctx* ctx, const void* rkeys, uint64_t nr, const void* skeys, uint64_t ns,

@@ -178,9 +178,9 @@ void check_key_bytes(uint32_t kb) {
 // LSD plans longer than CJ_MAX_PASSES (e.g. 20 bits at 1 bit/pass) run in
 // segments; each segment is itself stable, so the composition is the plan.
 void lsd_any(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, int kb,
-             const PassPlan& plan, const ValCols& vals) {
+             const PassPlan& plan, const ValCols& vals, unsigned long long* key_or = nullptr) {
   if (plan.npasses <= CJ_MAX_PASSES) {
-    lsd_partition(ctx, keys, keys_out, n, kb, plan, vals);
+    lsd_partition(ctx, keys, keys_out, n, kb, plan, vals, nullptr, key_or);
     return;
   }
   const void* cur = keys;
@@ -193,7 +193,7 @@ void lsd_any(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, int kb,
       seg.lo[i] = plan.lo[s + i];
       seg.hi[i] = plan.hi[s + i];
     }
-    lsd_partition(ctx, cur, keys_out, n, kb, seg, v);
+    lsd_partition(ctx, cur, keys_out, n, kb, seg, v, nullptr, s == 0 ? key_or : nullptr);
     cur = keys_out;
     for (int c = 0; c < v.n; ++c) v.in[c] = v.out[c];
     v.gen_ids = 0;
@@ -204,6 +204,7 @@ struct Side {
   void* keys = nullptr;
   void* cols[CJ_MAX_COLS + 1] = {};   // transformed carried columns
   uint64_t* offsets = nullptr;        // PHJ layout (device)
+  unsigned long long* key_or = nullptr;  // PHJ: OR of the keys (from the first histogram)
 };
 
 struct Timer {
@@ -279,11 +280,14 @@ Side transform(cj_ctx* ctx, const cj_relation* rel, int algo, bool gfur, unsigne
     if (total_bits == 0) {
       copy_columns(ctx, rel->key, s.keys, n, kb, v);
     } else {
+      s.key_or = static_cast<unsigned long long*>(ctx->alloc(8));
+      owned.push_back(s.key_or);
+      CJ_CUDA(cudaMemsetAsync(s.key_or, 0, 8, ctx->stream));
       // a hint wider than the partition bits says nothing about them
       lsd_any(ctx, rel->key, s.keys, n, kb,
               presorted > 0 && presorted <= total_bits
                   ? presorted_plan(total_bits, presorted, 6, bits_per_pass)
-                  : device_plan(total_bits, bits_per_pass), v);
+                  : device_plan(total_bits, bits_per_pass), v, s.key_or);
     }
     partition_offsets(ctx, s.keys, n, kb, total_bits, s.offsets);
   }
@@ -495,7 +499,7 @@ void run_join_dev(cj_ctx* ctx, const cj_relation* R, const cj_relation* S,
   auto count = [&]() -> uint64_t {
     if (opt->algo == CJ_SMJ) return smj_count(ctx, tr.keys, R->rows, ts.keys, S->rows, kb, pk_fk);
     return phj_count(ctx, tr.keys, tr.offsets, ts.keys, ts.offsets, fanout, kb,
-                     opt->sub_partition_limit);
+                     opt->sub_partition_limit, tr.key_or);
   };
   // PK-FK: at most one match per probe row (sized without a count pass); a
   // mislabelled build with duplicates overflows and is re-run exactly.
@@ -537,7 +541,7 @@ void run_join_dev(cj_ctx* ctx, const cj_relation* R, const cj_relation* S,
     if (opt->algo == CJ_SMJ)
       return smj_find(ctx, tr.keys, R->rows, ts.keys, S->rows, kb, pk_fk, o, capacity);
     return phj_find(ctx, tr.keys, tr.offsets, ts.keys, ts.offsets, fanout, kb,
-                    opt->sub_partition_limit, o, capacity);
+                    opt->sub_partition_limit, o, capacity, tr.key_or);
   };
   alloc_output(ctx, R, S, cap, want_ids || gfur, res);
   uint64_t total;

@@ -165,6 +165,12 @@ struct FindArgs {
   uint32_t off_e;            // stage offset of the match_e chunk
   int blocked;               // CTAs walk contiguous unit ranges (else round robin)
   uint32_t group;            // round robin over groups of this many consecutive units
+  // dense build keys: OR of the build keys (device); a unit whose table holds
+  // (OR >> dense_shift) + 1 slots addresses it directly by key >> dense_shift
+  // (the partition fixes the low dense_shift bits, so a unique key owns its
+  // slot: plain stores, one load per probe)
+  const unsigned long long* key_or;
+  uint32_t dense_shift;
 };
 
 // Multiplicative (Fibonacci) hashing as the reference's ChunkTable
@@ -697,6 +703,8 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
   uint32_t k = 0;
   int cb = 0;
   uint32_t cr = 0;
+  const uint64_t key_hi = a.key_or ? (uint64_t)(*a.key_or) >> a.dense_shift : ~0ull;
+  const uint32_t ds = a.dense_shift;
   for (uint64_t u = u_begin; u < u_end; u = next_u(u), ++k) {
     const int b = cb;
     const uint32_t cphase = cr;
@@ -762,14 +770,26 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
     //    The previous unit of this CTA left the same build chunk's table (or
     //    its sorted positions) in shared memory: reuse it.
     bool dup = false;
-    for (uint32_t i = reuse ? nb : tid; i < nb; i += kTmaThreads) {
-      const K key = bk[i];
-      uint32_t sl = slot_of(key, cap_log2);
-      while (true) {
-        const uint32_t old = atomicCAS(&tab[sl], kNoMatch, i);
-        if (old == kNoMatch) break;
-        if (bk[old] == key) dup = true;
-        sl = (sl + 1) & cmask;
+    // dense keys: slot = key >> dense_shift < cap for every build key
+    const bool dense = key_hi < cap;
+    if (dense) {
+      if (!reuse) {
+        for (uint32_t i = tid; i < nb; i += kTmaThreads) tab[(uint32_t)(bk[i] >> ds)] = i;
+        sync_c();
+        // equal keys share a slot: one of them does not find itself there
+        for (uint32_t i = tid; i < nb; i += kTmaThreads)
+          if (tab[(uint32_t)(bk[i] >> ds)] != i) dup = true;
+      }
+    } else {
+      for (uint32_t i = reuse ? nb : tid; i < nb; i += kTmaThreads) {
+        const K key = bk[i];
+        uint32_t sl = slot_of(key, cap_log2);
+        while (true) {
+          const uint32_t old = atomicCAS(&tab[sl], kNoMatch, i);
+          if (old == kNoMatch) break;
+          if (bk[old] == key) dup = true;
+          sl = (sl + 1) & cmask;
+        }
       }
     }
     if (dev::named_bar_or(1, kTmaThreads, dup)) s_dup = 1;
@@ -806,6 +826,20 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
     uint32_t wcount = 0;  // <= qchunk per unit
     uint16_t* const me_out = !WRITE && a.match_e ? a.match_e + inf.q_lo : nullptr;
     uint32_t r = r0;
+    if (!has_dup && dense) {
+      // direct-addressed table: the slot's entry is the match (same partition,
+      // same high bits: the same key)
+      for (; r < r1; ++r) {
+        const uint32_t jl = r * 32 + lane;
+        if (jl >= nq) continue;
+        const uint64_t hi = (uint64_t)(pk[jl] >> ds);
+        const uint32_t out = hi < cap ? tab[(uint32_t)hi] : kNoMatch;
+        const uint32_t m = out != kNoMatch;
+        if (WRITE) res[jl] = out;
+        else if (me_out) me_out[jl] = (uint16_t)(m ? out : kEmpty16);
+        wcount += m;
+      }
+    }
     if (!has_dup) {
       // four rounds at a time: the first table probe and the build-key check of
       // every round are independent loads (collisions take the loop)
@@ -1151,6 +1185,12 @@ FindArgs base_args(const void* bkeys, const uint64_t* boff, const void* pkeys,
   return a;
 }
 
+// CJ_DENSE=0 turns the direct-addressed tables off (experiments)
+bool dense_keys() {
+  const char* e = std::getenv("CJ_DENSE");
+  return !(e && std::strcmp(e, "0") == 0);
+}
+
 void check_limit(uint32_t limit) {
   if (limit == 0) fail(CJ_ERR_SPEC_INVALID, "sub-partition limit must be positive");
   if (limit > 16384)
@@ -1159,9 +1199,15 @@ void check_limit(uint32_t limit) {
 
 }  // namespace
 
+uint32_t log2_of(uint32_t fanout) {
+  uint32_t b = 0;
+  while ((1u << b) < fanout) ++b;
+  return b;
+}
+
 uint64_t phj_find(cj_ctx* ctx, const void* bkeys, const uint64_t* boff, const void* pkeys,
                   const uint64_t* poff, uint32_t fanout, int key_bytes, uint32_t limit,
-                  const OutSpec& out, uint64_t capacity) {
+                  const OutSpec& out, uint64_t capacity, const unsigned long long* key_or) {
   check_limit(limit);
   Scratch us(ctx, sizeof(uint64_t) * ((uint64_t)fanout + 1));
   Plan plan = make_plan(ctx, boff, poff, fanout, limit, us.as<uint64_t>(), probe_chunk());
@@ -1169,6 +1215,8 @@ uint64_t phj_find(cj_ctx* ctx, const void* bkeys, const uint64_t* boff, const vo
   a.unit_start = us.as<uint64_t>();
   a.max_chunk = (uint32_t)std::max<uint64_t>(plan.max_chunk, 1);
   a.write = 1;
+  a.key_or = dense_keys() ? key_or : nullptr;
+  a.dense_shift = log2_of(fanout);
   a.capacity = capacity;
   a.padded = out.padded ? 1 : 0;
   a.nb_rows = out.r_rows;
@@ -1215,7 +1263,8 @@ uint64_t phj_find(cj_ctx* ctx, const void* bkeys, const uint64_t* boff, const vo
 }
 
 uint64_t phj_count(cj_ctx* ctx, const void* bkeys, const uint64_t* boff, const void* pkeys,
-                   const uint64_t* poff, uint32_t fanout, int key_bytes, uint32_t limit) {
+                   const uint64_t* poff, uint32_t fanout, int key_bytes, uint32_t limit,
+                   const unsigned long long* key_or) {
   check_limit(limit);
   Scratch us(ctx, sizeof(uint64_t) * ((uint64_t)fanout + 1));
   const Plan plan = make_plan(ctx, boff, poff, fanout, limit, us.as<uint64_t>(), probe_chunk());
@@ -1223,6 +1272,8 @@ uint64_t phj_count(cj_ctx* ctx, const void* bkeys, const uint64_t* boff, const v
   a.unit_start = us.as<uint64_t>();
   a.max_chunk = (uint32_t)std::max<uint64_t>(plan.max_chunk, 1);
   a.write = 0;
+  a.key_or = dense_keys() ? key_or : nullptr;
+  a.dense_shift = log2_of(fanout);
   return key_bytes == 4 ? run_find<uint32_t>(ctx, a, plan.total_units)
                         : run_find<uint64_t>(ctx, a, plan.total_units);
 }

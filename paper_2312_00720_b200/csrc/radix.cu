@@ -44,6 +44,7 @@ struct HistArgs {
   uint32_t nblocks, hparts;
   uint32_t lowbits;  // shard mode: digit = shard << lowbits | low key bits
   uint32_t shift[8], mask[8];
+  unsigned long long* key_or;  // optional: OR of every key (the join's dense-key test)
 };
 
 // Digit width: 8 bits (256 digits) everywhere, or 9 bits (512) for the
@@ -81,7 +82,9 @@ k_block_hist(const K* __restrict__ keys, const __grid_constant__ HistArgs a,
     shf[p] = a.shift[p];
     msk[p] = a.mask[p];
   }
+  K kor = 0;
   auto count = [&](K k) {
+    kor |= k;
     if (SHARD) {
       atomicAdd(&mine[dev::shard_digit((uint64_t)k, a.hparts, a.lowbits)], 1u);
     } else {
@@ -117,6 +120,12 @@ k_block_hist(const K* __restrict__ keys, const __grid_constant__ HistArgs a,
     i = lo + nvec * kVec;
   }
   for (uint64_t j = i + threadIdx.x; j < hi; j += kHistThreads) count(keys[j]);
+  if (a.key_or) {
+    uint64_t o = (uint64_t)kor;
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) o |= __shfl_xor_sync(0xffffffffu, o, s);
+    if ((threadIdx.x & 31) == 0 && o) atomicOr(a.key_or, (unsigned long long)o);
+  }
   __syncthreads();
   for (int d = threadIdx.x; d < kWidth; d += kHistThreads) {
     uint32_t t = 0;
@@ -438,11 +447,16 @@ __global__ void k_offsets(const K* __restrict__ keys, uint64_t n, uint32_t bits,
 //      re-staging barrier.
 // Global row indices are u32 (kMaxRows = 2^31 - 1, column.hpp:21).
 
-template <int RANK>
+// mm: the warp's peer-mask row of (1 << RB) + 32 words.  Lanes that take no
+// part OR zero into a word of their own past the digit words: a predicated
+// atomic may be issued for every lane (an OR with 0 changes nothing), and the
+// idle lanes of a skewed pass — a dominant digit handled by ballot — must not
+// all hit one word (30 serialised wavefronts per atomic, profiles/r02_*).
+template <int RANK, int RB>
 __device__ __forceinline__ uint32_t peers_of(uint32_t d, bool valid, uint32_t* mm, uint32_t bits) {
   const uint32_t lane = threadIdx.x & 31u;
   if (RANK == 0) {
-    if (valid) atomicOr(&mm[d], 1u << lane);
+    atomicOr(valid ? &mm[d] : &mm[(1u << RB) + lane], valid ? 1u << lane : 0u);
     __syncwarp();
     const uint32_t p = valid ? mm[d] : 0u;
     __syncwarp();
@@ -510,10 +524,10 @@ __device__ __forceinline__ void scatter_tile(const BlockPassArgs& a, const uint8
     if constexpr (HOT) {
       const bool h = valid && d == hot;
       const uint32_t hb = __ballot_sync(0xffffffffu, h);
-      peers = peers_of<RANK>(d, valid && !h, mm, a.bits);
+      peers = peers_of<RANK, RB>(d, valid && !h, mm, a.bits);
       if (h) peers = hb;
     } else {
-      peers = peers_of<RANK>(d, valid, mm, a.bits);
+      peers = peers_of<RANK, RB>(d, valid, mm, a.bits);
     }
     const uint32_t lt = peers & dev::lanemask_lt();
     uint32_t old = 0;
@@ -671,7 +685,7 @@ k_scatter_v2(const __grid_constant__ BlockPassArgs a) {
   uint8_t* const stage0 = smem;
   uint16_t* const sidx = reinterpret_cast<uint16_t*>(smem + (size_t)a.stages * a.stage_bytes);
   // per-warp peer masks (rank mode 0) after the source indices, 16-byte aligned
-  uint32_t (*match_word)[kR] = reinterpret_cast<uint32_t (*)[kR]>(
+  uint32_t (*match_word)[kR + 32] = reinterpret_cast<uint32_t (*)[kR + 32]>(
       smem + (((size_t)a.stages * a.stage_bytes + (size_t)kTile * 2 + 15) & ~size_t(15)));
   __shared__ uint16_t whist[(NT / 32)][kR];
   __shared__ uint32_t dstart[kR];
@@ -707,7 +721,7 @@ k_scatter_v2(const __grid_constant__ BlockPassArgs a) {
     if (t_begin < t_end && full_tile(t_begin)) issue(0, t_begin);
   }
   if (RANK == 0)
-    for (int i = tid; i < (NT / 32) * kR; i += NT) (&match_word[0][0])[i] = 0;
+    for (int i = tid; i < (NT / 32) * (kR + 32); i += NT) (&match_word[0][0])[i] = 0;
   __shared__ uint64_t s_dmax[kR / 32];
   if (tid < kR) {
     uint64_t c = a.base[tid];
@@ -877,7 +891,7 @@ ScatterGeom scatter_geom(cj_ctx* ctx, uint64_t n, int key_bytes, const ValCols& 
   // ~4 KB of cursors, twice that for 9-bit digits) and the dynamic peer masks
   // of rank mode 0 (16 KB / 32 KB)
   const size_t budget = (227 / g.ctas_per_sm - (((size_t)12 << rb) >> 8)) * 1024;
-  const size_t match = g.rank == 0 ? (size_t)(g.threads / 32) * 4 << rb : 0;
+  const size_t match = g.rank == 0 ? (size_t)(g.threads / 32) * 4 * ((1u << rb) + 32) : 0;
   for (int items : {16, 12, 8, 4}) {
     if (items > want_items && items > 4) continue;
     if (rb == 9 && items > 12) continue;
@@ -900,7 +914,8 @@ ScatterGeom scatter_geom(cj_ctx* ctx, uint64_t n, int key_bytes, const ValCols& 
 }
 
 void block_hist(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes, const PassPlan& plan,
-                const ScatterGeom& g, uint32_t* cnt_dev, uint32_t hparts, uint32_t lowbits) {
+                const ScatterGeom& g, uint32_t* cnt_dev, uint32_t hparts, uint32_t lowbits,
+                unsigned long long* key_or) {
   const int np = plan.npasses;
   if (np < 1 || np > 8) fail(CJ_ERR_UNSUPPORTED, "histogram of 1..8 passes");
   HistArgs a{};
@@ -910,6 +925,7 @@ void block_hist(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes, const 
   a.nblocks = g.nblocks;
   a.hparts = hparts;
   a.lowbits = lowbits;
+  a.key_or = key_or;
   for (int p = 0; p < np; ++p) {
     a.shift[p] = plan.lo[p];
     a.mask[p] = (1u << (plan.hi[p] - plan.lo[p])) - 1u;
@@ -936,10 +952,11 @@ void block_hist(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes, const 
 void histogram_passes(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes,
                       const PassPlan& plan, const ScatterGeom& g, uint32_t* cnt_dev,
                       uint32_t* totals_dev, uint64_t* base_dev,
-                      std::vector<uint32_t>* totals_host, uint32_t hparts, uint32_t lowbits) {
+                      std::vector<uint32_t>* totals_host, uint32_t hparts, uint32_t lowbits,
+                      unsigned long long* key_or) {
   const int np = plan.npasses;
   if (np > 8) fail(CJ_ERR_UNSUPPORTED, "histogram of more than 8 passes");
-  block_hist(ctx, keys, n, key_bytes, plan, g, cnt_dev, hparts, lowbits);
+  block_hist(ctx, keys, n, key_bytes, plan, g, cnt_dev, hparts, lowbits, key_or);
   const uint32_t R = 1u << g.rb;
   ctx->kbegin("digit_bases", 12ull * R * np);
   k_digit_bases<<<1, 1024, 0, ctx->stream>>>(cnt_dev, g.nblocks, np, R, totals_dev, base_dev);
@@ -1063,7 +1080,7 @@ void copy_columns(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, int
 namespace {
 void lsd_partition_group(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, int key_bytes,
                          const PassPlan& plan, const ValCols& vals,
-                         std::vector<uint32_t>* counts_out);
+                         std::vector<uint32_t>* counts_out, unsigned long long* key_or);
 }  // namespace
 
 // Wide rows are partitioned in column groups of at most 32 payload bytes: each
@@ -1071,12 +1088,13 @@ void lsd_partition_group(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t
 // permutation (the reference re-partitions each GFTR payload column with the key
 // the same way, join_engine.cpp:180-213).
 void lsd_partition(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, int key_bytes,
-                   const PassPlan& plan, const ValCols& vals, std::vector<uint32_t>* counts_out) {
+                   const PassPlan& plan, const ValCols& vals, std::vector<uint32_t>* counts_out,
+                   unsigned long long* key_or) {
   constexpr uint32_t kGroupBytes = 32;
   uint32_t total = 0;
   for (int c = 0; c < vals.n; ++c) total += vals.bytes[c];
-  if (total <= kGroupBytes) return lsd_partition_group(ctx, keys, keys_out, n, key_bytes, plan, vals,
-                                                       counts_out);
+  if (total <= kGroupBytes)
+    return lsd_partition_group(ctx, keys, keys_out, n, key_bytes, plan, vals, counts_out, key_or);
   int c = 0;
   bool first = true;
   while (c < vals.n) {
@@ -1091,7 +1109,8 @@ void lsd_partition(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, in
       ++c;
     }
     g.gen_ids = first ? vals.gen_ids : 0;
-    lsd_partition_group(ctx, keys, keys_out, n, key_bytes, plan, g, first ? counts_out : nullptr);
+    lsd_partition_group(ctx, keys, keys_out, n, key_bytes, plan, g, first ? counts_out : nullptr,
+                        first ? key_or : nullptr);
     first = false;
   }
 }
@@ -1099,7 +1118,7 @@ void lsd_partition(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, in
 namespace {
 void lsd_partition_group(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, int key_bytes,
                          const PassPlan& plan, const ValCols& vals,
-                         std::vector<uint32_t>* counts_out) {
+                         std::vector<uint32_t>* counts_out, unsigned long long* key_or) {
   if (plan.npasses > 8) fail(CJ_ERR_UNSUPPORTED, "LSD segment longer than 8 passes");
   const int np = plan.npasses;
   // digit tables sized to the widest pass: 64 digits for passes of <= 6 bits
@@ -1122,7 +1141,7 @@ void lsd_partition_group(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t
   // (ctx->assume_live_passes) run every pass instead and save the sync.
   const bool skip_check = ctx->assume_live_passes && !counts_out;
   histogram_passes(ctx, keys, n, key_bytes, plan, g0, cnt.as<uint32_t>(), tot.as<uint32_t>(),
-                   base.as<uint64_t>(), skip_check ? nullptr : &totals);
+                   base.as<uint64_t>(), skip_check ? nullptr : &totals, 0, 0, key_or);
   if (counts_out) *counts_out = totals;
   std::vector<int> live;
   for (int p = 0; p < np; ++p) {
