@@ -170,7 +170,7 @@ void histogram_passes(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes,
 void scatter_pass(cj_ctx* ctx, const void* keys_in, void* keys_out, uint64_t n, int key_bytes,
                   uint32_t lo, uint32_t hi, const uint64_t* base_dev, const uint32_t* cnt,
                   uint32_t cnt_stride, const ScatterGeom& g, const ValCols& vals,
-                  uint32_t hparts = 0, uint32_t lowbits = 0);
+                  uint32_t hparts = 0, uint32_t lowbits = 0, int runs = 0);
 
 // Stable partition of rows by digit = shard << lowbits | (key & (2^lowbits - 1)),
 // shard = floor(mix64(key) * parts / 2^64) (the multi-GPU shuffle's send

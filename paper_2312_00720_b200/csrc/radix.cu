@@ -20,6 +20,8 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <cstdio>
+#include <vector>
 
 #include "cj_device.cuh"
 #include "cj_internal.cuh"
@@ -401,12 +403,14 @@ struct BlockPassArgs {
   uint32_t shift, mask, bits;
   uint32_t hparts;          // > 0: digit = shard of the key << lowbits | its low lowbits bits
   uint32_t lowbits;
+  int runs;                 // input grouped by an earlier pass: test rounds for one digit
   const uint64_t* base;     // [256] exclusive digit base of this pass
   const uint32_t* cnt;      // per-block counts of this pass: cnt[b * cnt_stride + d]
   uint32_t cnt_stride;
   uint32_t stage_bytes, pbytes;
   int nvals, gen_ids;
   int stages;               // 2: prefetch the next tile while this one runs
+  unsigned long long* cta_ns;  // CJ_CTA_TIMES: [start, end] globaltimer per CTA (diagnostics)
   const void* vin[CJ_MAX_COLS + 1];
   void* vout[CJ_MAX_COLS + 1];
   uint32_t vbytes[CJ_MAX_COLS + 1];
@@ -447,16 +451,20 @@ __global__ void k_offsets(const K* __restrict__ keys, uint64_t n, uint32_t bits,
 //      re-staging barrier.
 // Global row indices are u32 (kMaxRows = 2^31 - 1, column.hpp:21).
 
-// mm: the warp's peer-mask row of (1 << RB) + 32 words.  Lanes that take no
-// part OR zero into a word of their own past the digit words: a predicated
-// atomic may be issued for every lane (an OR with 0 changes nothing), and the
-// idle lanes of a skewed pass — a dominant digit handled by ballot — must not
-// all hit one word (30 serialised wavefronts per atomic, profiles/r02_*).
+// mm: the warp's peer-mask row of (1 << RB) + 32 words (the 32 spare words
+// are unused: kept so the table layout does not depend on the rank mode).
 template <int RANK, int RB>
 __device__ __forceinline__ uint32_t peers_of(uint32_t d, bool valid, uint32_t* mm, uint32_t bits) {
   const uint32_t lane = threadIdx.x & 31u;
   if (RANK == 0) {
-    atomicOr(valid ? &mm[d] : &mm[(1u << RB) + lane], valid ? 1u << lane : 0u);
+    // a truly predicated shared reduction: lanes that take no part issue
+    // nothing (an if-converted atomicOr(.., 0) from every lane costs ~18
+    // wavefronts in a skewed round: profiles/r02_scatter_skew_atoms.txt)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t"
+        "@p red.shared.or.b32 [%0], %1;\n\t}" ::"r"(dev::smem_addr(&mm[d])),
+        "r"(1u << lane), "r"((uint32_t)valid)
+        : "memory");
     __syncwarp();
     const uint32_t p = valid ? mm[d] : 0u;
     __syncwarp();
@@ -494,10 +502,10 @@ __device__ __forceinline__ uint32_t digit_of(K k, const BlockPassArgs& a) {
 }
 
 // One tile of k_scatter_v2 (phases 1-4).  FULL: tile_n == kTile, no guards.
-// HOT: the pass has one dominant digit `hot` (skewed keys): its lanes take
-// their peer mask from one ballot instead of an atomic OR on a single shared
-// word that a third or more of every warp would hit.
-template <class K, int ITEMS, int RANK, bool SHARD, bool FULL, int RB, bool HOT, int NT>
+// HOT (skewed keys): the pass has one dominant digit `hot` (>= 1/8 of the
+// rows).  Its lanes take their peer masks from a ballot instead of an atomic
+// OR on a shared word that much of the warp would hit.
+template <class K, int ITEMS, int RANK, bool SHARD, bool FULL, int RB, int HOT, bool UNI, int NT>
 __device__ __forceinline__ void scatter_tile(const BlockPassArgs& a, const uint8_t* st,
                                              uint16_t* sidx, uint16_t (*whist)[1 << RB],
                                              uint32_t* mm, uint32_t* dstart, uint32_t* run,
@@ -521,7 +529,25 @@ __device__ __forceinline__ void scatter_tile(const BlockPassArgs& a, const uint8
     const bool valid = FULL || li < tile_n;
     const uint32_t d = digit_of<SHARD>(skey[li], a);
     uint32_t peers;
-    if constexpr (HOT) {
+    // After a first pass over skewed keys the rows arrive grouped by its
+    // digit, so a frequent key's rows are contiguous and most lanes of a round
+    // share one digit: they would serialise on one shared word.  UNI: the
+    // lanes holding lane 0's digit take their peer mask from one ballot, the
+    // others the atomic-OR masks (a second leader measured slower; per-CTA
+    // times: profiles/r02_skew_summary.md).
+    if constexpr (UNI) {
+      const uint32_t d0 = __shfl_sync(0xffffffffu, d, 0);
+      const bool m0 = valid && d == d0;
+      const uint32_t b0 = __ballot_sync(0xffffffffu, m0);
+      if (b0 == 0xffffffffu) {
+        peers = b0;
+      } else {
+        peers = peers_of<RANK, RB>(d, valid && !m0, mm, a.bits);
+        if (m0) peers = b0;
+      }
+    } else if constexpr (HOT) {
+      // a dominant digit (>= 1/8 of the rows): its lanes take one ballot, the
+      // others the atomic-OR masks
       const bool h = valid && d == hot;
       const uint32_t hb = __ballot_sync(0xffffffffu, h);
       peers = peers_of<RANK, RB>(d, valid && !h, mm, a.bits);
@@ -741,7 +767,12 @@ k_scatter_v2(const __grid_constant__ BlockPassArgs a) {
   // >= 1/8 of the rows: a warp round holds 4+ lanes of that digit on average
   const uint32_t hot = !SHARD && RANK == 0 && (vmax >> 16) * 8 >= a.n ? (uint32_t)(vmax & 0xffffu)
                                                                          : 0xffffffffu;
+  // skewed digits after an earlier pass (the top digit at least twice its
+  // uniform share): frequent keys arrive in runs, test rounds for one digit
+  const bool uni = !SHARD && RANK == 0 && a.runs && ((vmax >> 16) << a.bits) >= 2 * a.n;
 
+  uint64_t t_start = 0;
+  if (a.cta_ns && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   uint32_t ph0 = 0, ph1 = 0;
   int b = 0;
   uint32_t* mm = &match_word[RANK == 0 ? warp : 0][0];
@@ -764,12 +795,16 @@ k_scatter_v2(const __grid_constant__ BlockPassArgs a) {
     if (full_tile(t)) {
       dev::mbar_wait(&mbar[b], b ? ph1 : ph0);
       if (b) ph1 ^= 1; else ph0 ^= 1;
-      if (hot != 0xffffffffu)
-        scatter_tile<K, ITEMS, RANK, SHARD, true, RB, true, NT>(a, st, sidx, whist, mm, dstart, run, goff,
-                                                            wsum, (uint32_t)tbase, tile_n, hot);
-      else
-        scatter_tile<K, ITEMS, RANK, SHARD, true, RB, false, NT>(a, st, sidx, whist, mm, dstart, run, goff,
-                                                             wsum, (uint32_t)tbase, tile_n, hot);
+#define CJ_TILE(H, U)                                                                      \
+  scatter_tile<K, ITEMS, RANK, SHARD, true, RB, H, U, NT>(a, st, sidx, whist, mm, dstart, run, goff, \
+                                                          wsum, (uint32_t)tbase, tile_n, hot)
+      switch ((hot != 0xffffffffu ? 1 : 0) | (uni ? 2 : 0)) {
+        case 0: CJ_TILE(0, false); break;
+        case 1: CJ_TILE(1, false); break;
+        case 2: CJ_TILE(0, true); break;
+        default: CJ_TILE(1, true); break;
+      }
+#undef CJ_TILE
     } else {  // last, partial tile: plain loads
       K* wk = reinterpret_cast<K*>(st);
       for (uint32_t j = tid; j < kTile; j += NT) wk[j] = j < tile_n ? kin[tbase + j] : K(0);
@@ -786,7 +821,7 @@ k_scatter_v2(const __grid_constant__ BlockPassArgs a) {
         }
       }
       __syncthreads();
-      scatter_tile<K, ITEMS, RANK, SHARD, false, RB, false, NT>(a, st, sidx, whist, mm, dstart, run, goff,
+      scatter_tile<K, ITEMS, RANK, SHARD, false, RB, 0, false, NT>(a, st, sidx, whist, mm, dstart, run, goff,
                                                             wsum, (uint32_t)tbase, tile_n, hot);
     }
     __syncthreads();
@@ -794,6 +829,12 @@ k_scatter_v2(const __grid_constant__ BlockPassArgs a) {
       dev::fence_proxy_async();
       issue(0, t + 1);
     }
+  }
+  if (a.cta_ns && tid == 0) {
+    uint64_t t_end_ns;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end_ns));
+    a.cta_ns[2 * blockIdx.x] = t_start;
+    a.cta_ns[2 * blockIdx.x + 1] = t_end_ns;
   }
 }
 
@@ -974,7 +1015,7 @@ void histogram_passes(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes,
 void scatter_pass(cj_ctx* ctx, const void* keys_in, void* keys_out, uint64_t n, int key_bytes,
                   uint32_t lo, uint32_t hi, const uint64_t* base_dev, const uint32_t* cnt,
                   uint32_t cnt_stride, const ScatterGeom& g, const ValCols& vals, uint32_t hparts,
-                  uint32_t lowbits) {
+                  uint32_t lowbits, int runs) {
   if (n == 0) return;
   if (hparts && !g.tma)
     fail(CJ_ERR_UNSUPPORTED, "shard partition needs 16-byte aligned columns");
@@ -996,6 +1037,7 @@ void scatter_pass(cj_ctx* ctx, const void* keys_in, void* keys_out, uint64_t n, 
     a.mask = (1u << (hi - lo)) - 1u;
     a.hparts = hparts;
     a.lowbits = lowbits;
+    a.runs = runs;
     if (hparts) {  // digit = shard << lowbits | low bits: ceil(log2 parts) + lowbits bits
       uint32_t sb = 0;
       while ((1u << sb) < hparts) ++sb;
@@ -1015,6 +1057,9 @@ void scatter_pass(cj_ctx* ctx, const void* keys_in, void* keys_out, uint64_t n, 
       a.vbytes[c] = vals.bytes[c];
       a.voff[c] = g.voff[c];
     }
+    static const bool cta_times = std::getenv("CJ_CTA_TIMES") != nullptr;
+    Scratch cta_buf(ctx, cta_times ? 16ull * g.nblocks : 0);
+    a.cta_ns = cta_times ? cta_buf.as<unsigned long long>() : nullptr;
     ctx->kbegin("scatter_pass", n * (row + wrow));
     if (key_bytes == 4) {
       if (g.rank == 1) launch_v2_items<uint32_t, 1>(ctx, a, g.smem, g.items, g.rb, g.threads);
@@ -1025,6 +1070,26 @@ void scatter_pass(cj_ctx* ctx, const void* keys_in, void* keys_out, uint64_t n, 
     }
     ctx->kend();
     CJ_CUDA(cudaGetLastError());
+    if (cta_times) {  // diagnostics: per-CTA durations of this pass (stderr)
+      std::vector<unsigned long long> h(2ull * g.nblocks);
+      CJ_CUDA(cudaMemcpyAsync(h.data(), cta_buf.p, 16ull * g.nblocks, cudaMemcpyDeviceToHost,
+                              ctx->stream));
+      CJ_CUDA(cudaStreamSynchronize(ctx->stream));
+      unsigned long long t0 = ~0ull, t1 = 0;
+      std::vector<double> d(g.nblocks);
+      for (uint32_t i = 0; i < g.nblocks; ++i) {
+        t0 = std::min(t0, h[2 * i]);
+        t1 = std::max(t1, h[2 * i + 1]);
+        d[i] = (h[2 * i + 1] - h[2 * i]) / 1e3;
+      }
+      std::vector<double> sd = d;
+      std::sort(sd.begin(), sd.end());
+      std::fprintf(stderr, "cta_times n=%llu bits=%u..%u: span %.1f us, per-CTA min %.1f med %.1f max %.1f us; first 16:",
+                   (unsigned long long)n, lo, hi, (t1 - t0) / 1e3, sd.front(), sd[sd.size() / 2],
+                   sd.back());
+      for (uint32_t i = 0; i < g.nblocks; i += std::max(1u, g.nblocks / 16)) std::fprintf(stderr, " %.0f", d[i]);
+      std::fprintf(stderr, "\n");
+    }
     return;
   }
   // fallback for unaligned columns: register-staged onesweep with look-back
@@ -1182,10 +1247,12 @@ void lsd_partition_group(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t
     for (int c = 0; c < nv; ++c) step.out[c] = to_out ? vals.out[c] : scratch_cols[c];
     step.gen_ids = li == 0 ? vals.gen_ids : 0;
     const uint64_t* pbase = base.as<uint64_t>() + (size_t)p * kRadix;
+    // after an earlier pass (or a presorted first digit) the rows arrive in runs
+    const int runs = li > 0 || plan.done > 0;
     if (li == 0) {
       scatter_pass(ctx, cur_k, tk, n, key_bytes, plan.lo[p], plan.hi[p], pbase,
                    g0.tma ? cnt.as<uint32_t>() + (size_t)p * kRadix : nullptr,
-                   (uint32_t)(kRadix * np), g0, step);
+                   (uint32_t)(kRadix * np), g0, step, 0, 0, runs);
     } else {
       const ScatterGeom g = scatter_geom(ctx, n, key_bytes, step, cur_k, rb);
       const uint32_t* pc = nullptr;
@@ -1200,7 +1267,7 @@ void lsd_partition_group(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t
         pc = cnt2.as<uint32_t>();
       }
       scatter_pass(ctx, cur_k, tk, n, key_bytes, plan.lo[p], plan.hi[p], pbase, pc, kRadix, g,
-                   step);
+                   step, 0, 0, runs);
     }
     cur_k = tk;
     for (int c = 0; c < nv; ++c) cur.in[c] = step.out[c];
