@@ -109,6 +109,11 @@ def parse():
                         "shard partition, the NCCL exchange and the per-rank join)")
     p.add_argument("--no-configs", action="store_true",
                    help="skip the C3/C4 records (PHJ/SMJ-GFTR, 3 timed steps each)")
+    p.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                   help="weak: every rank joins a C2-sized shard (the default line); strong: "
+                        "a fixed C2 x 2^strong-log2 join split over the ranks (sharded path)")
+    p.add_argument("--strong-log2", type=int, default=2,
+                   help="strong scaling total = C2 x 2^k (k=2: 2^29 x 2^30, fits one GPU)")
     p.add_argument("--e2e-steps", type=int, default=32,
                    help="end-to-end steps (two lanes; more steps amortise the lanes' ramp)")
     return p.parse_args()
@@ -182,8 +187,11 @@ class Clocks:
 
 def config_dict(cfg, a, nr, ns, world):
     """The `config` object of the JSON line; both arms print the same one."""
-    sharded = world > 1 or a.sharded
-    if sharded:
+    sharded = world > 1 or a.sharded or a.scaling == "strong"
+    if sharded and a.scaling == "strong":
+        wl = (f"C5-shaped strong scaling: |R|=2^{27 + a.strong_log2}, |S|=2^{28 + a.strong_log2} "
+              f"total over {world} GPU(s), 4-byte key + 2 x 4-byte payloads, cj_gen_shard")
+    elif sharded:
         wl = (f"C5-shaped weak scaling: |R|={world}x2^27, |S|={world}x2^28 total, 4-byte key + "
               "2 x 4-byte payloads, cj_gen_shard")
     else:
@@ -247,6 +255,8 @@ def reference_arm(a):
     world = max(world, a.gpus)
     # the whole job: under N ranks our arm joins N C2-sized shards (weak scaling)
     nr, ns = (cfg["r"] >> a.scale_log2) * world, (cfg["s"] >> a.scale_log2) * world
+    if a.scaling == "strong":  # the same fixed total as our strong-scaling line
+        nr, ns = (cfg["r"] >> a.scale_log2) << a.strong_log2, (cfg["s"] >> a.scale_log2) << a.strong_log2
     cores = os.cpu_count() or 1
     env = dict(os.environ, OMP_NUM_THREADS=str(cores))
 
@@ -276,7 +286,7 @@ def reference_arm(a):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "tuples/s", "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u64" if cfg["key"] == 8 else "u32",
+        "scaling": a.scaling, "vs_baseline": None, "dtype": "u64" if cfg["key"] == 8 else "u32",
         "data": "synthetic: the reference's workloads::gen_pk_fk (seed 42), on the host",
         "config": config_dict(cfg, a, cfg["r"] >> a.scale_log2, cfg["s"] >> a.scale_log2, world),
         "same_workload": shift == 0,
@@ -331,7 +341,7 @@ def main():
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
-    sharded = world > 1 or a.sharded
+    sharded = world > 1 or a.sharded or a.scaling == "strong"
     out_fd = None
     if sharded:
         # rank 0 prints exactly one JSON line: NCCL's banner and anything else a
@@ -382,7 +392,12 @@ def main():
         # weak scaling: every rank owns a C2-sized slice of a world-times larger
         # PK-FK join; rows are shuffled to their key's shard over NCCL
         from paper_2312_00720_b200 import distributed as D
-        R, S = D.gen_shard(ctx, nr * world, ns * world, rank, world, NPAY, NPAY, SEED)
+        if a.scaling == "strong":  # a fixed total split over the ranks
+            tot_r, tot_s = nr << a.strong_log2, ns << a.strong_log2
+            nr, ns = tot_r // world, tot_s // world
+        else:
+            tot_r, tot_s = nr * world, ns * world
+        R, S = D.gen_shard(ctx, tot_r, tot_s, rank, world, NPAY, NPAY, SEED)
         comm = D.Comm.from_group(ctx)
 
         def step():
@@ -503,7 +518,7 @@ def main():
         balg = b_alg_star(algo, pattern, ns, nr, cfg["dims"])
     out = {
         "metric": METRIC, "value": value, "unit": "tuples/s", "n_gpus": world, "steps": a.steps,
-        "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": a.scaling,
         "vs_baseline": None, "dtype": "u64" if cfg["key"] == 8 else "u32",
         "data": "synthetic: bit-identical to the reference's workloads::gen_pk_fk "
                 "(seed 42 + rank), generated on the device",
