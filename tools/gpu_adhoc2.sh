@@ -1,2 +1,3 @@
 cd $GRAFT_REPO_ROOT 2>/dev/null || cd /root/repo
-for c in C4z1.5 C4z1.0; do echo "== $c"; CJ_CTA_TIMES=1 CONFIG=$c timeout 300 python tools/diag.py phj-gftr 2>&1 | grep "cta_times n=268\| 3 wall" | tail -4; done
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q > /tmp/t.log 2>&1; tail -3 /tmp/t.log
+for env in CJ_LOOKBACK=1 CJ_LOOKBACK=0; do echo "== $env"; for c in C2 C4z1.5 C3; do env $env CONFIG=$c timeout 300 python tools/diag.py phj-gftr smj-gftr 2>&1 | grep " 3 wall"; done; done
