@@ -232,7 +232,7 @@ constexpr uint64_t kPad = 64;
 uint64_t phj_find(cj_ctx* ctx, const void* bkeys, const uint64_t* boff, const void* pkeys,
                   const uint64_t* poff, uint32_t fanout, int key_bytes, uint32_t limit,
                   const OutSpec& out, uint64_t capacity,
-                  const unsigned long long* key_or = nullptr);
+                  const unsigned long long* key_or = nullptr, bool pk_fk = false);
 // Match count only (for sizing outputs), plus optional per-reference-unit counts.
 uint64_t phj_count(cj_ctx* ctx, const void* bkeys, const uint64_t* boff, const void* pkeys,
                    const uint64_t* poff, uint32_t fanout, int key_bytes, uint32_t limit,

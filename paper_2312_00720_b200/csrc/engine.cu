@@ -541,7 +541,7 @@ void run_join_dev(cj_ctx* ctx, const cj_relation* R, const cj_relation* S,
     if (opt->algo == CJ_SMJ)
       return smj_find(ctx, tr.keys, R->rows, ts.keys, S->rows, kb, pk_fk, o, capacity);
     return phj_find(ctx, tr.keys, tr.offsets, ts.keys, ts.offsets, fanout, kb,
-                    opt->sub_partition_limit, o, capacity, tr.key_or);
+                    opt->sub_partition_limit, o, capacity, tr.key_or, pk_fk);
   };
   alloc_output(ctx, R, S, cap, want_ids || gfur, res);
   uint64_t total;

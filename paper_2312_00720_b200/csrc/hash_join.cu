@@ -171,6 +171,11 @@ struct FindArgs {
   // slot: plain stores, one load per probe)
   const unsigned long long* key_or;
   uint32_t dense_shift;
+  // speculative PK-FK fill (no count pass): every unit expects each probe row
+  // to match once and writes at its probe offset; a unit that finds a miss or
+  // a duplicate build key sets *spec_fail, later units stop, and the caller
+  // runs count + fill
+  uint32_t* spec_fail;
 };
 
 // Multiplicative (Fibonacci) hashing as the reference's ChunkTable
@@ -572,6 +577,7 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
   __shared__ __align__(8) uint64_t full[2], empty[2];
   __shared__ uint64_t s_wcnt[2][kTmaWarps], s_wb[2][kTmaWarps];  // by unit parity
   __shared__ int s_dup;
+  __shared__ int s_abort[2];  // speculative fill: the producer stopped at this stage
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t units = a.n_units;
@@ -641,7 +647,7 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
       p.d = descs[uu];
       p.dup = WRITE && a.match_e != nullptr ? a.unit_dup[uu] : 1u;
       p.cnt = WRITE && a.unit_counts ? a.unit_counts[uu] : ~0ull;
-      p.base = WRITE && a.unit_off ? a.unit_off[uu] : 0ull;
+      p.base = WRITE && a.spec_fail ? p.d.q_lo : (WRITE && a.unit_off ? a.unit_off[uu] : 0ull);
       return p;
     };
     Pf nx{};
@@ -660,6 +666,13 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
         pr ^= 1u;
       }
       const UnitDesc d = cur.d;
+      if (WRITE && a.spec_fail && *reinterpret_cast<volatile uint32_t*>(a.spec_fail)) {
+        // a unit failed the speculation: wake the consumers on this stage and stop
+        s_abort[b] = 1;
+        dev::mbar_arrive(&full[b]);
+        return;
+      }
+      s_abort[b] = 0;
       // pre: the count pass resolved this unit's matches (match_e); no build keys needed
       const bool pre = WRITE && cur.dup == 0;
       s_desc[b] = d;
@@ -715,6 +728,7 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
     uint64_t* s_wcount = s_wcnt[k & 1u];
     uint64_t* s_wbase = s_wb[k & 1u];
     dev::mbar_wait(&full[b], cphase);
+    if (WRITE && s_abort[b]) break;
     const UnitDesc inf = s_desc[b];
     const bool pre = s_pre[b];
     const bool reuse = inf.b_lo == built_lo && inf.b_hi == built_hi;
@@ -926,6 +940,17 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
     }
     if (!WRITE) continue;
     sync_c();
+    if (a.spec_fail) {
+      // speculation: this unit's rows go to its probe offset only if every
+      // probe row matched exactly once
+      const uint64_t got = s_wbase[kTmaWarps - 1] + s_wcount[kTmaWarps - 1] - s_ubase[b];
+      if (has_dup || got != nq) {
+        if (tid == 0) atomicExch(a.spec_fail, 1u);
+        release(b);
+        sync_c();
+        continue;
+      }
+    }
 
     // 3. emit finished rows in probe order at the unit's offset
     const uint32_t bsh4 = (uint32_t)(inf.b_lo & 3), bsh8 = (uint32_t)(inf.b_lo & 1);
@@ -1075,6 +1100,29 @@ uint64_t run_find(cj_ctx* ctx, FindArgs a, uint64_t total_units) {
     // count pass (keys only) -> scan -> fill pass; no inter-CTA waiting
     const uint64_t U = total_units;
     uint64_t total = 0;
+    if (U > 0 && a.write && a.spec_fail) {
+      // PK-FK speculation: one fill pass, each unit at its probe offset
+      FindArgs as = a;
+      as.match_e = nullptr;
+      as.unit_dup = nullptr;
+      as.unit_counts = nullptr;
+      as.unit_off = nullptr;
+      size_t smem_s = 0;
+      tma_layout<K>(as, &smem_s);
+      const unsigned grid =
+          (unsigned)std::min<uint64_t>((uint64_t)ctx->num_sms * find_ctas_per_sm(), U);
+      CJ_CUDA(cudaFuncSetAttribute(k_phj_tma<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem_s));
+      ctx->kbegin("phj_find", 0);
+      k_phj_tma<K, true><<<grid, kTmaThreads + 32, smem_s, ctx->stream>>>(as);
+      ctx->kend();
+      CJ_CUDA(cudaGetLastError());
+      uint32_t* h = ctx->host_pinned;
+      CJ_CUDA(cudaMemcpyAsync(h, a.spec_fail, 4, cudaMemcpyDeviceToHost, ctx->stream));
+      CJ_CUDA(cudaStreamSynchronize(ctx->stream));
+      if (h[0] == 0) return a.np_rows;  // every probe row matched once
+    }
+    a.spec_fail = nullptr;
     if (U > 0) {
       Scratch counts(ctx, U * 8), offs(ctx, U * 8);
       FindArgs ac = a;
@@ -1207,7 +1255,8 @@ uint32_t log2_of(uint32_t fanout) {
 
 uint64_t phj_find(cj_ctx* ctx, const void* bkeys, const uint64_t* boff, const void* pkeys,
                   const uint64_t* poff, uint32_t fanout, int key_bytes, uint32_t limit,
-                  const OutSpec& out, uint64_t capacity, const unsigned long long* key_or) {
+                  const OutSpec& out, uint64_t capacity, const unsigned long long* key_or,
+                  bool pk_fk) {
   check_limit(limit);
   Scratch us(ctx, sizeof(uint64_t) * ((uint64_t)fanout + 1));
   Plan plan = make_plan(ctx, boff, poff, fanout, limit, us.as<uint64_t>(), probe_chunk());
@@ -1217,6 +1266,11 @@ uint64_t phj_find(cj_ctx* ctx, const void* bkeys, const uint64_t* boff, const vo
   a.write = 1;
   a.key_or = dense_keys() ? key_or : nullptr;
   a.dense_shift = log2_of(fanout);
+  // speculate that every probe row finds its key (PK-FK): skips the count
+  // pass when it holds (C2, C4); a miss falls back to count + fill
+  const char* se = std::getenv("CJ_SPECULATE");
+  if (pk_fk && capacity >= out.s_rows && !(se && std::strcmp(se, "0") == 0))
+    a.spec_fail = ctx->ticket(3);
   a.capacity = capacity;
   a.padded = out.padded ? 1 : 0;
   a.nb_rows = out.r_rows;
