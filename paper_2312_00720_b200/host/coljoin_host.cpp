@@ -20,6 +20,7 @@
 #include "coljoin/hash_match.hpp"
 #include "coljoin/join_engine.hpp"
 #include "coljoin/sequence.hpp"
+#include "coljoin/sharded.hpp"
 #include "coljoin/merge_match.hpp"
 #include "coljoin/primitives.hpp"
 
@@ -701,15 +702,14 @@ Relation output_shell(uint64_t rows, const Relation& r, const Relation& s) {
 
 }  // namespace
 
-JoinOutput run_join(const JoinTask& task) {
-  if (!task.build || !task.probe) throw SpecInvalid("join task needs both input relations");
+namespace detail {
+
+// Shared by run_join and sharded::run_join: upload, one C-ABI join call,
+// download of the output relation and the report.
+template <class Call>
+JoinOutput run_join_with(const JoinTask& task, Call&& call, const char* what) {
   const Relation& r = *task.build;
   const Relation& s = *task.probe;
-  if (r.key.kind() != s.key.kind()) throw KindError("build and probe key kinds differ");
-  if (task.options.radix_bits_per_pass == 0 || task.options.radix_bits_per_pass > 8)
-    throw FanoutTooLarge("radix bits per pass must be in [1, 8]");
-  if (r.payloads.size() > CJ_MAX_COLS || s.payloads.size() > CJ_MAX_COLS)
-    throw Unsupported("at most 16 payload columns per relation");
   auto& d = Device::get();
   std::lock_guard<std::mutex> lock(d.mu());
   std::vector<Buf> rc = upload_relation(r), sc = upload_relation(s);
@@ -725,7 +725,7 @@ JoinOutput run_join(const JoinTask& task) {
   opt.want_stats = 1;  // JoinStats (join_engine.hpp:54-58) is part of the result
   cj_join_result res;
   std::memset(&res, 0, sizeof(res));
-  d.check(cj_run_join(d.ctx(), &R, &S, &opt, &res), "run_join");
+  d.check(call(d.ctx(), &R, &S, &opt, &res), what);
   struct Release {
     cj_join_result* r;
     ~Release() { cj_result_free(Device::get().ctx(), r); }
@@ -750,6 +750,24 @@ JoinOutput run_join(const JoinTask& task) {
   out.stats.clusteredness_s = res.clusteredness_s;
   return out;
 }
+
+}  // namespace detail
+
+JoinOutput run_join(const JoinTask& task) {
+  if (!task.build || !task.probe) throw SpecInvalid("join task needs both input relations");
+  const Relation& r = *task.build;
+  const Relation& s = *task.probe;
+  if (r.key.kind() != s.key.kind()) throw KindError("build and probe key kinds differ");
+  if (task.options.radix_bits_per_pass == 0 || task.options.radix_bits_per_pass > 8)
+    throw FanoutTooLarge("radix bits per pass must be in [1, 8]");
+  if (r.payloads.size() > CJ_MAX_COLS || s.payloads.size() > CJ_MAX_COLS)
+    throw Unsupported("at most 16 payload columns per relation");
+  return detail::run_join_with(task, [](cj_ctx* ctx, const cj_relation* R, const cj_relation* S,
+                                         const cj_join_options* opt, cj_join_result* res) {
+    return cj_run_join(ctx, R, S, opt, res);
+  }, "run_join");
+}
+
 
 std::vector<SequenceStep> run_join_sequence(const Relation& fact, const std::vector<Relation>& dims,
                                             JoinAlgo algorithm, JoinPattern pattern,
@@ -913,4 +931,52 @@ void materialize_gftr(const MatchSet& match, const Relation& r, const Relation& 
   materialize_gftr(match.ids_r, match.ids_s, r, s, std::move(fr), std::move(fs), ctx, out);
 }
 
+
+namespace sharded {
+
+CommId make_comm_id() {
+  CommId id{};
+  const int st = cj_comm_unique_id(id.data());
+  if (st != CJ_OK) detail::throw_status(st, "comm id (NCCL unavailable?)");
+  return id;
+}
+
+Comm::Comm(const CommId& id, int nranks, int rank) {
+  auto& d = detail::Device::get();
+  d.check(cj_comm_init(d.ctx(), id.data(), nranks, rank, &comm_), "comm init");
+}
+
+Comm::~Comm() { cj_comm_destroy(comm_); }
+int Comm::size() const { return cj_comm_size(comm_); }
+int Comm::rank() const { return cj_comm_rank(comm_); }
+
+JoinOutput run_join(const JoinTask& task, Comm& comm, ShuffleStats* stats) {
+  if (!task.build || !task.probe) throw SpecInvalid("join task needs both input relations");
+  if (task.build->key.kind() != task.probe->key.kind())
+    throw KindError("build and probe key kinds differ");
+  if (task.options.radix_bits_per_pass == 0 || task.options.radix_bits_per_pass > 8)
+    throw FanoutTooLarge("radix bits per pass must be in [1, 8]");
+  cj_shuffle_stats st{};
+  JoinOutput out = detail::run_join_with(
+      task,
+      [&](cj_ctx* ctx, const cj_relation* R, const cj_relation* S, const cj_join_options* opt,
+          cj_join_result* res) {
+        return cj_run_join_sharded(ctx, comm.handle(), R, S, opt, res, &st);
+      },
+      "run_join_sharded");
+  if (stats) {
+    stats->first_bits = st.first_bits;
+    stats->r_rows_received = st.r_rows_received;
+    stats->s_rows_received = st.s_rows_received;
+    stats->bytes_sent_peers = st.bytes_sent_peers;
+    stats->bytes_received_peers = st.bytes_received_peers;
+    stats->shard_ns = st.shard_ns;
+    stats->exchange_r_ns = st.exchange_r_ns;
+    stats->exchange_s_ns = st.exchange_s_ns;
+    stats->wall_ns = st.wall_ns;
+  }
+  return out;
+}
+
+}  // namespace sharded
 }  // namespace coljoin
