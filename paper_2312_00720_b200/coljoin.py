@@ -116,7 +116,10 @@ class DeviceBuffer:
 
     def __del__(self):
         if self.ptr and self.ctx.h:
-            A.lib().cj_free(self.ctx.h, C.c_void_p(self.ptr))
+            try:
+                A.lib().cj_free(self.ctx.h, C.c_void_p(self.ptr))
+            except (TypeError, AttributeError):  # interpreter shutdown: modules torn down
+                pass
             self.ptr = 0
 
 

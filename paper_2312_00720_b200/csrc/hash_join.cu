@@ -428,6 +428,7 @@ constexpr int kTmaWarps = kTmaThreads / 32;
 
 struct UnitDesc {
   uint64_t b_lo, b_hi, q_lo, q_hi;
+  uint32_t split;  // the partition holds more build rows than the limit (several build chunks)
 };
 
 // One thread per unit: its partition by binary search over unit_start (a
@@ -453,6 +454,7 @@ __global__ void k_phj_desc(const uint64_t* __restrict__ boff, const uint64_t* __
     d.b_hi = dev::umin64(b1, d.b_lo + limit);
     d.q_lo = q0 + (l % nqc) * qchunk;
     d.q_hi = dev::umin64(q1, d.q_lo + qchunk);
+    d.split = b1 - b0 > limit ? 1u : 0u;
     desc[u] = d;
   }
 }
@@ -809,7 +811,10 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
     if (dev::named_bar_or(1, kTmaThreads, dup)) s_dup = 1;
     sync_c();
     const bool has_dup = s_dup != 0;
-    if (!WRITE && a.unit_dup && tid == 0) a.unit_dup[u] = has_dup ? 1 : 0;
+    // a probe row of a split partition meets several build chunks, one unit
+    // each, and matches in at most one: its match index cannot be handed to
+    // the fill (the fill rebuilds those units' tables)
+    if (!WRITE && a.unit_dup && tid == 0) a.unit_dup[u] = has_dup || inf.split ? 1 : 0;
     uint16_t* sidx = reinterpret_cast<uint16_t*>(tab);
     built_lo = inf.b_lo;
     built_hi = inf.b_hi;
@@ -838,7 +843,7 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
 
     // 2. probe from shared memory; warp w owns a contiguous run of rounds
     uint32_t wcount = 0;  // <= qchunk per unit
-    uint16_t* const me_out = !WRITE && a.match_e ? a.match_e + inf.q_lo : nullptr;
+    uint16_t* const me_out = !WRITE && a.match_e && !inf.split ? a.match_e + inf.q_lo : nullptr;
     uint32_t r = r0;
     if (!has_dup && dense) {
       // direct-addressed table: the slot's entry is the match (same partition,

@@ -741,7 +741,18 @@ size_t smj_layout(SmjArgs& a, bool write, int stages = 2) {
 }
 
 template <class K>
+uint64_t run(cj_ctx* ctx, SmjArgs a);
+
+template <class K>
 uint64_t run_tma(cj_ctx* ctx, SmjArgs a) {
+  if (a.write) {
+    // rows too wide for two staged 2048-row probe tiles (many payload
+    // columns): the general kernel, which reads the columns in place
+    SmjArgs t = a;
+    t.match_e = reinterpret_cast<uint16_t*>(16);  // the widest layout (with the hand-off)
+    t.nstages = 2;
+    if (smj_layout_w<K>(t, true, 512) > 220 * 1024) return run<K>(ctx, a);
+  }
   a.tiles = (a.ns + kTileS - 1) / kTileS;
   Scratch tot(ctx, 8);
   CJ_CUDA(cudaMemsetAsync(tot.p, 0, 8, ctx->stream));

@@ -463,3 +463,23 @@ def test_ledger_zero_rows(ctx):
     Sd = cj.Relation(cj.to_device(e), [cj.to_device(e)], "S", False)
     out = cj.run_join(ctx, Rd, Sd, "phj", "gftr")
     assert out.report.column_bytes[0] == 0 and out.report.column_bytes[2] == 0
+
+
+@pytest.mark.parametrize("algo_bits,limit", [(2, 4096), (4, 1024), (6, 4096)])
+@pytest.mark.parametrize("pattern", ["gftr", "gfur"])
+@pytest.mark.parametrize("match", [1.0, 0.6])
+def test_phj_build_partitions_above_the_limit(ctx, algo_bits, limit, pattern, match):
+    """Partitions holding more build rows than the sub-partition limit split into
+    several build chunks (hash_match.cpp:186-210): every probe chunk meets every
+    build chunk of its partition.  Exact rows and order against the oracle."""
+    R, S = O.gen_pk_fk(1 << 16, 1 << 17, 2, 1, match=match, seed=31 + algo_bits)
+    Rd = cj.Relation(cj.to_device(R["key"]), [cj.to_device(p) for p in R["payloads"]], "R", True)
+    Sd = cj.Relation(cj.to_device(S["key"]), [cj.to_device(p) for p in S["payloads"]], "S", False)
+    out = cj.run_join(ctx, Rd, Sd, "phj", pattern, total_radix_bits=algo_bits,
+                      sub_partition_limit=limit)
+    ref = O.run_join(R, S, "phj", pattern, total_bits=algo_bits, limit=limit)
+    got = [H(out.relation.key)] + [H(p) for p in out.relation.payloads]
+    want = [ref["key"]] + ref["payloads"]
+    assert out.matches == len(ref["key"])
+    for g, w in zip(got, want):
+        assert np.array_equal(g, w.astype(np.uint64))
