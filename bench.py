@@ -89,6 +89,7 @@ def gen_config(ctx, cfg, nr, ns):
             return [c if w == 8 else c.view(torch.int32)[::2].contiguous() for c, w in zip(cols, ws)]
         R = cj.Relation(R.key, narrow(R.payloads), "R", True)
         S = cj.Relation(S.key, narrow(S.payloads), "S", False)
+        torch.cuda.synchronize()  # the narrowing copies ran on torch's stream
     return R, S
 
 

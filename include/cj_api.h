@@ -63,6 +63,9 @@ typedef struct cj_ctx cj_ctx;
 /* stream: a cudaStream_t (NULL = a new non-blocking stream owned by the ctx). */
 int cj_ctx_create(int device, void* stream, cj_ctx** out);
 int cj_ctx_destroy(cj_ctx* ctx);
+/* The cudaStream_t the ctx works on (callers order their own streams
+ * against it, e.g. torch.cuda.ExternalStream + wait_stream). */
+void* cj_ctx_stream(const cj_ctx* ctx);
 const char* cj_last_error(const cj_ctx* ctx);
 int cj_sync(cj_ctx* ctx);
 int cj_free(cj_ctx* ctx, void* dev_ptr);

@@ -106,6 +106,7 @@ _U64P = C.POINTER(C.c_uint64)
 PROTOS = {
     "cj_ctx_create": (C.c_int, [C.c_int, _P, C.POINTER(_P)]),
     "cj_ctx_destroy": (C.c_int, [_P]),
+    "cj_ctx_stream": (_P, [_P]),
     "cj_last_error": (C.c_char_p, [_P]),
     "cj_sync": (C.c_int, [_P]),
     "cj_free": (C.c_int, [_P, _P]),

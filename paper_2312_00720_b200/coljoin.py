@@ -69,6 +69,9 @@ class Context:
         if st != 0:
             raise A._BY_CODE.get(st, A.Error)(f"cj_ctx_create failed (status {st})")
         self.h = h
+        # the library's own stream (a fresh non-blocking one unless a stream
+        # was passed): torch work is ordered against it by `fenced`
+        self.lib_stream = torch.cuda.ExternalStream(A.lib().cj_ctx_stream(h) or 0, device=device)
 
     @property
     def launches(self) -> int:
@@ -93,6 +96,27 @@ class Context:
 
     def __exit__(self, *exc):
         self.close()
+
+
+def fenced(fn):
+    """Entry points that take a Context first: the library's stream waits for
+    the work torch queued on its current stream (the inputs), and torch's
+    stream waits for the library's work (the outputs), without host syncs."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapper(ctx, *args, **kw):
+        torch = _torch()
+        lib = getattr(ctx, "lib_stream", None)
+        if lib is None:
+            return fn(ctx, *args, **kw)
+        cur = torch.cuda.current_stream(ctx.device)
+        lib.wait_stream(cur)
+        try:
+            return fn(ctx, *args, **kw)
+        finally:
+            cur.wait_stream(lib)
+    return wrapper
 
 
 class DeviceBuffer:
@@ -143,6 +167,7 @@ def _empty(n, nbytes):
 
 # ---- primitives (primitives.hpp:25-77) --------------------------------------
 
+@fenced
 def histogram(ctx: Context, keys, low_bit: int, high_bit: int) -> np.ndarray:
     fan = 1 << max(0, min(high_bit - low_bit, 8))
     out = (C.c_uint32 * fan)()
@@ -159,6 +184,7 @@ def exclusive_prefix_sum(counts) -> np.ndarray:
     return out
 
 
+@fenced
 def radix_partition(ctx: Context, keys, vals: Sequence, low_bit: int, high_bit: int):
     """One stable pass; returns (keys_out, [vals_out], offsets[np.uint64])."""
     n = keys.numel()
@@ -176,6 +202,7 @@ def radix_partition(ctx: Context, keys, vals: Sequence, low_bit: int, high_bit: 
     return ko, vo, np.frombuffer(off, dtype=np.uint64).copy()
 
 
+@fenced
 def radix_partition_passes(ctx: Context, keys, vals: Sequence, plan, gen_ids: bool = False):
     n = keys.numel()
     ko = _empty(n, _nbytes(keys))
@@ -191,6 +218,7 @@ def radix_partition_passes(ctx: Context, keys, vals: Sequence, plan, gen_ids: bo
     return ko, vo
 
 
+@fenced
 def sort_pairs(ctx: Context, keys, vals: Sequence = (), gen_ids: bool = False):
     n = keys.numel()
     ko = _empty(n, _nbytes(keys))
@@ -207,6 +235,7 @@ def sort_keys(ctx: Context, keys):
     return sort_pairs(ctx, keys, ())[0]
 
 
+@fenced
 def gather(ctx: Context, cols: Sequence, idx):
     """out[c][i] = cols[c][idx[i]]; idx int32 tensor of u32 ids."""
     m = idx.numel()
@@ -227,6 +256,7 @@ def gather_clusteredness(ids: np.ndarray) -> float:
     return float(np.abs(np.diff(ids.astype(np.int64))).sum()) / (ids.size - 1)
 
 
+@fenced
 def partition_relation(ctx: Context, keys, vals: Sequence, total_bits: int,
                        bits_per_pass: int = 8, gen_ids: bool = False):
     """hash_match.hpp:26-38; returns (keys_out, [vals_out], offsets device int64)."""
@@ -244,6 +274,7 @@ def partition_relation(ctx: Context, keys, vals: Sequence, total_bits: int,
     return ko, vo, off
 
 
+@fenced
 def hash_find_matches(ctx: Context, bkeys, boff, pkeys, poff, limit: int = 4096,
                       id_mode: str = "virtual", bcarried=None, pcarried=None):
     """hash_match.hpp:73-81: returns (keys, ids_r, ids_s) device tensors."""
@@ -264,6 +295,7 @@ def hash_find_matches(ctx: Context, bkeys, boff, pkeys, poff, limit: int = 4096,
             _wrap(ctx, js.value, t, 4))
 
 
+@fenced
 def merge_find_matches(ctx: Context, r_sorted, s_sorted, pk_fk: bool, validate: bool = False):
     """merge_match.hpp:49-52: returns (keys, ids_r, ids_s) device tensors."""
     if _nbytes(r_sorted) != _nbytes(s_sorted):
@@ -380,6 +412,7 @@ def join_output(ctx: Context, res, R, S, build: Relation, probe: Relation, kw) -
                       res.clusteredness_s if kw.get("want_stats") else 1.0, ids_r, ids_s)
 
 
+@fenced
 def run_join(ctx: Context, build: Relation, probe: Relation, algo="phj", pattern="gftr",
              **kw) -> JoinOutput:
     """join_engine.hpp:68 run_join on device-resident relations."""
@@ -391,6 +424,7 @@ def run_join(ctx: Context, build: Relation, probe: Relation, algo="phj", pattern
     return join_output(ctx, res, R, S, build, probe, kw)
 
 
+@fenced
 def run_join_presorted(ctx: Context, build: Relation, probe: Relation, presorted_bits: int,
                        algo="phj", pattern="gftr", **kw) -> JoinOutput:
     """run_join on relations already stably grouped by their low
@@ -423,6 +457,7 @@ class _HostArena:
         raise KeyError(ptr)
 
 
+@fenced
 def run_join_host(ctx: Context, build: Relation, probe: Relation, algo="phj", pattern="gftr",
                   **kw):
     """The drop-in for coljoin::run_join(const JoinTask&) with host columns:
@@ -452,6 +487,7 @@ def run_join_host(ctx: Context, build: Relation, probe: Relation, algo="phj", pa
 
 # ---- workloads (workloads.hpp:11-33) ------------------------------------------
 
+@fenced
 def gen_pk_fk(ctx: Context, r_rows, s_rows, r_payloads=1, s_payloads=1, key_bytes=4,
               pay_bytes=4, match_ratio=1.0, zipf_factor=0.0, seed=0):
     """Device-resident inputs bit-identical to workloads::gen_pk_fk."""
@@ -474,6 +510,7 @@ class SequenceStep:
     fk_fetch_ns: int
 
 
+@fenced
 def run_join_sequence(ctx: Context, fact: Relation, dims: Sequence, algo="phj", pattern="gftr",
                       **kw):
     """sequence.hpp:21-24 run_join_sequence, device-resident (no host copy
@@ -502,6 +539,7 @@ def run_join_sequence(ctx: Context, fact: Relation, dims: Sequence, algo="phj", 
                              PhaseReport(res.transform_ns, res.find_ns, res.materialize_ns), t)
 
 
+@fenced
 def gen_star(ctx: Context, fact_rows: int, dims: int, dim_rows: int, seed: int = 0,
              key_bytes: int = 4, pay_bytes: int = 4):
     """workloads.hpp:47-61 gen_star, bit-identical, on the device."""

@@ -715,6 +715,8 @@ uint32_t* cj_ctx::ticket(int slot) {
 
 extern "C" {
 
+void* cj_ctx_stream(const cj_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
 int cj_ctx_create(int device, void* stream, cj_ctx** out) {
   if (!out) return CJ_ERR_SPEC_INVALID;
   *out = nullptr;

@@ -74,6 +74,7 @@ class Comm:
         self.close()
 
 
+@cj.fenced
 def shard_partition(ctx, rel, parts: int, first_bits: int = 0):
     """Device send layout: rows stably grouped by (shard, low first_bits key
     bits); counts[dst][d] as a (parts, 2^first_bits) array."""
@@ -124,6 +125,7 @@ def stats_dict(st: A.ShuffleStats) -> dict:
     return {f: getattr(st, f) for f, _ in A.ShuffleStats._fields_}
 
 
+@cj.fenced
 def shuffle(ctx, comm: Comm, rel, first_bits: int = 0, stats: Optional[dict] = None):
     """This rank's shard of `rel` from every rank (cj_shuffle_relation), stably
     grouped by its low first_bits key bits."""
@@ -140,6 +142,7 @@ def shuffle(ctx, comm: Comm, rel, first_bits: int = 0, stats: Optional[dict] = N
     return cj.Relation(key, pays, rel.name, rel.key_unique)
 
 
+@cj.fenced
 def distributed_join(ctx, build, probe, algo="phj", pattern="gftr", comm: Optional[Comm] = None,
                      timings: Optional[dict] = None, **kw):
     """Join this rank's slices of R and S across the communicator's ranks
@@ -157,6 +160,7 @@ def distributed_join(ctx, build, probe, algo="phj", pattern="gftr", comm: Option
     return cj.join_output(ctx, res, R, S, build, probe, kw)
 
 
+@cj.fenced
 def gen_shard(ctx, r_rows_total, s_rows_total, rank, ranks, r_payloads=2, s_payloads=2, seed=42):
     """This rank's slice of the weak-scaling workload (cj_gen_shard)."""
     rn, sn = r_rows_total // ranks, s_rows_total // ranks

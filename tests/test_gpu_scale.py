@@ -143,6 +143,7 @@ def test_full_size_digest_matches_reference(name, golden):
                     for c, w in zip(cols, widths)]
         R = cj.Relation(R.key, narrow(R.payloads), "R", True)
         S = cj.Relation(S.key, narrow(S.payloads), "S", False)
+        torch.cuda.synchronize()  # the narrowing copies ran on torch's stream
     for algo, pattern in (("phj", "gftr"), ("smj", "gftr"), ("phj", "gfur"), ("smj", "gfur"),
                           ("nphj", "gftr")):
         out = cj.run_join(ctx, R, S, algo, pattern)

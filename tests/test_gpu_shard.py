@@ -141,6 +141,8 @@ def test_sharded_join_equals_single_join(ctx, world, algo, pattern):
                 lo = int(so[d, dg])
                 for c, col in enumerate([rel.key] + list(rel.payloads)):
                     cols[c][ro[src, dg]:ro[src, dg] + n] = col[lo:lo + n]
+        # the copies run on torch's stream, the join on the library's
+        torch.cuda.current_stream().synchronize()
         return cj.Relation(cols[0], cols[1:], side, side == "R")
 
     got = []
@@ -154,6 +156,7 @@ def test_sharded_join_equals_single_join(ctx, world, algo, pattern):
                        [cat([R.payloads[c] for R, _ in slices]) for c in range(2)], "R", True)
     Sall = cj.Relation(cat([S.key for _, S in slices]),
                        [cat([S.payloads[c] for _, S in slices]) for c in range(2)], "S", False)
+    torch.cuda.current_stream().synchronize()
     single = cj.run_join(ctx, Rall, Sall, algo, pattern)
     assert union[0].size == single.matches == ns
     assert O.canonical_digest(union) == O.canonical_digest(
