@@ -720,6 +720,11 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
   uint32_t cr = 0;
   const uint64_t key_hi = a.key_or ? (uint64_t)(*a.key_or) >> a.dense_shift : ~0ull;
   const uint32_t ds = a.dense_shift;
+  // Direct-addressed tables hold (tag << 16) | chunk index; a new build chunk
+  // takes a new tag, so the table is cleared only when the region was last
+  // used otherwise (CAS table, sorted positions) or the tags wrap.
+  uint32_t utag = 0;
+  bool tab_tagged = false;
   for (uint64_t u = u_begin; u < u_end; u = next_u(u), ++k) {
     const int b = cb;
     const uint32_t cphase = cr;
@@ -775,9 +780,21 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
     // smallest power of two >= 2 nb (at least 2)
     const uint32_t cap_log2 = nb <= 1 ? 1u : 33u - (uint32_t)__clz(nb - 1);
     const uint32_t cap = 1u << cap_log2, cmask = cap - 1;
+    // dense keys: slot = key >> dense_shift < cap for every build key
+    const bool dense = key_hi < cap;
     if (!reuse) {
       if (tid == 0) s_dup = 0;
-      for (uint32_t i = tid; i < cap; i += kTmaThreads) tab[i] = kNoMatch;
+      if (dense) {
+        if (!tab_tagged || utag == 0xfffeu) {
+          for (uint32_t i = tid; i < a.cap_entries; i += kTmaThreads) tab[i] = 0;
+          utag = 0;
+          tab_tagged = true;
+        }
+        ++utag;
+      } else {
+        for (uint32_t i = tid; i < cap; i += kTmaThreads) tab[i] = kNoMatch;
+        tab_tagged = false;
+      }
     }
     sync_c();
 
@@ -786,15 +803,14 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
     //    The previous unit of this CTA left the same build chunk's table (or
     //    its sorted positions) in shared memory: reuse it.
     bool dup = false;
-    // dense keys: slot = key >> dense_shift < cap for every build key
-    const bool dense = key_hi < cap;
+    const uint32_t tagged = utag << 16;
     if (dense) {
       if (!reuse) {
-        for (uint32_t i = tid; i < nb; i += kTmaThreads) tab[(uint32_t)(bk[i] >> ds)] = i;
+        for (uint32_t i = tid; i < nb; i += kTmaThreads) tab[(uint32_t)(bk[i] >> ds)] = tagged | i;
         sync_c();
         // equal keys share a slot: one of them does not find itself there
         for (uint32_t i = tid; i < nb; i += kTmaThreads)
-          if (tab[(uint32_t)(bk[i] >> ds)] != i) dup = true;
+          if (tab[(uint32_t)(bk[i] >> ds)] != (tagged | i)) dup = true;
       }
     } else {
       for (uint32_t i = reuse ? nb : tid; i < nb; i += kTmaThreads) {
@@ -818,6 +834,7 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
     uint16_t* sidx = reinterpret_cast<uint16_t*>(tab);
     built_lo = inf.b_lo;
     built_hi = inf.b_hi;
+    if (has_dup) tab_tagged = false;  // the region holds sorted positions now
     if (has_dup && !reuse) {  // stably sorted chunk positions: bitonic over (key, position)
       uint32_t np2 = 1;
       while (np2 < nb) np2 <<= 1;
@@ -852,8 +869,9 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
         const uint32_t jl = r * 32 + lane;
         if (jl >= nq) continue;
         const uint64_t hi = (uint64_t)(pk[jl] >> ds);
-        const uint32_t out = hi < cap ? tab[(uint32_t)hi] : kNoMatch;
-        const uint32_t m = out != kNoMatch;
+        const uint32_t e = hi < cap ? tab[(uint32_t)hi] : 0u;
+        const uint32_t m = (e >> 16) == utag;
+        const uint32_t out = m ? (e & 0xffffu) : kNoMatch;
         if (WRITE) res[jl] = out;
         else if (me_out) me_out[jl] = (uint16_t)(m ? out : kEmpty16);
         wcount += m;
