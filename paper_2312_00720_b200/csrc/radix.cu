@@ -404,6 +404,7 @@ struct BlockPassArgs {
   uint32_t hparts;          // > 0: digit = shard of the key << lowbits | its low lowbits bits
   uint32_t lowbits;
   int runs;                 // input grouped by an earlier pass: test rounds for one digit
+  int warp_slots;           // phase 4: warp-contiguous slots instead of CTA-strided
   const uint64_t* base;     // [256] exclusive digit base of this pass
   const uint32_t* cnt;      // per-block counts of this pass: cnt[b * cnt_stride + d]
   uint32_t cnt_stride;
@@ -657,27 +658,31 @@ __device__ __forceinline__ void scatter_tile(const BlockPassArgs& a, const uint8
   CJ_CLK(1);
 
   // 4. write key + carried columns of each slot (loads batched for ILP)
+  // slot of item k: warp-contiguous (a warp writes 32*ITEMS consecutive slots,
+  // a.warp_slots) or CTA-strided (slot tid + k*NT)
+  const uint32_t jb = a.warp_slots ? (uint32_t)warp * 32 * ITEMS + lane : (uint32_t)tid;
+  const uint32_t js = a.warp_slots ? 32u : (uint32_t)NT;
   uint32_t src[ITEMS], g[ITEMS];
   K key[ITEMS];
 #pragma unroll
   for (int k = 0; k < ITEMS; ++k) {
-    const uint32_t j = tid + k * NT;
+    const uint32_t j = jb + k * js;
     src[k] = (FULL || j < tile_n) ? sidx[j] : 0u;
   }
 #pragma unroll
   for (int k = 0; k < ITEMS; ++k) key[k] = skey[src[k]];
 #pragma unroll
-  for (int k = 0; k < ITEMS; ++k) g[k] = goff[digit_of<SHARD>(key[k], a)] + tid + k * NT;
+  for (int k = 0; k < ITEMS; ++k) g[k] = goff[digit_of<SHARD>(key[k], a)] + jb + k * js;
   K* __restrict__ kout = static_cast<K*>(a.keys_out);
 #pragma unroll
   for (int k = 0; k < ITEMS; ++k)
-    if (FULL || tid + k * NT < tile_n) kout[g[k]] = key[k];
+    if (FULL || jb + k * js < tile_n) kout[g[k]] = key[k];
   for (int c = 0; c < a.nvals; ++c) {
     if (a.gen_ids && c == 0) {
       uint32_t* __restrict__ vout = static_cast<uint32_t*>(a.vout[c]);
 #pragma unroll
       for (int k = 0; k < ITEMS; ++k)
-        if (FULL || tid + k * NT < tile_n) vout[g[k]] = tbase + src[k];
+        if (FULL || jb + k * js < tile_n) vout[g[k]] = tbase + src[k];
     } else if (a.vbytes[c] == 4) {
       const uint32_t* sv = reinterpret_cast<const uint32_t*>(st + a.voff[c]);
       uint32_t* __restrict__ vout = static_cast<uint32_t*>(a.vout[c]);
@@ -686,7 +691,7 @@ __device__ __forceinline__ void scatter_tile(const BlockPassArgs& a, const uint8
       for (int k = 0; k < ITEMS; ++k) v[k] = sv[src[k]];
 #pragma unroll
       for (int k = 0; k < ITEMS; ++k)
-        if (FULL || tid + k * NT < tile_n) vout[g[k]] = v[k];
+        if (FULL || jb + k * js < tile_n) vout[g[k]] = v[k];
     } else {
       const uint64_t* sv = reinterpret_cast<const uint64_t*>(st + a.voff[c]);
       uint64_t* __restrict__ vout = static_cast<uint64_t*>(a.vout[c]);
@@ -695,7 +700,7 @@ __device__ __forceinline__ void scatter_tile(const BlockPassArgs& a, const uint8
       for (int k = 0; k < ITEMS; ++k) v[k] = sv[src[k]];
 #pragma unroll
       for (int k = 0; k < ITEMS; ++k)
-        if (FULL || tid + k * NT < tile_n) vout[g[k]] = v[k];
+        if (FULL || jb + k * js < tile_n) vout[g[k]] = v[k];
     }
   }
   CJ_CLK(7);
@@ -1038,6 +1043,14 @@ void scatter_pass(cj_ctx* ctx, const void* keys_in, void* keys_out, uint64_t n, 
     a.hparts = hparts;
     a.lowbits = lowbits;
     a.runs = runs;
+    // phase-4 slot order: warp-contiguous for 64-digit passes (longer runs per
+    // warp: C2 PHJ scatter 6.17 -> 6.04 ms), CTA-strided for wider digits
+    // (SMJ 7-bit passes 9.01 -> 9.17 ms the other way); CJ_SLOTS=warp|cta forces
+    static const int slots_env = [] {
+      const char* e = std::getenv("CJ_SLOTS");
+      return e ? (std::strcmp(e, "warp") == 0 ? 1 : 0) : -1;
+    }();
+    a.warp_slots = slots_env >= 0 ? slots_env : (g.rb <= 6 ? 1 : 0);
     if (hparts) {  // digit = shard << lowbits | low bits: ceil(log2 parts) + lowbits bits
       uint32_t sb = 0;
       while ((1u << sb) < hparts) ++sb;
