@@ -657,6 +657,11 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
     uint32_t k = 0;
     int pb = 0;
     uint32_t pr = 0;
+    // the build chunk each stage buffer holds (keys and R payloads stay valid
+    // there: later units on that stage overwrite only their probe regions), so
+    // the units of one build chunk that land on the same stage copy it once
+    uint64_t st_lo[4] = {~0ull, ~0ull, ~0ull, ~0ull}, st_hi[4] = {0, 0, 0, 0};
+    bool st_keys[4] = {false, false, false, false};
     for (uint64_t u = u_begin; u < u_end; u = next_u(u), ++k) {
       const Pf cur = nx;
       if (next_u(u) < u_end) nx = fetch(next_u(u));
@@ -684,10 +689,17 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
         s_ubase[b] = cur.base;
       }
       uint8_t* st = smem + (size_t)b * a.stage_bytes;
+      const bool same = st_lo[b] == d.b_lo && st_hi[b] == d.b_hi;
+      const bool need_keys = !pre && !(same && st_keys[b]);
+      const bool need_r = WRITE && !same;
+      st_keys[b] = same ? (st_keys[b] || !pre) : !pre;
+      st_lo[b] = d.b_lo;
+      st_hi[b] = d.b_hi;
       uint32_t total = bytes(d.q_lo, d.q_hi, kb);
-      if (!pre) total += bytes(d.b_lo, d.b_hi, kb);
+      if (need_keys) total += bytes(d.b_lo, d.b_hi, kb);
       if (WRITE) {
-        for (int c = 0; c < a.nr; ++c) total += bytes(d.b_lo, d.b_hi, a.r_bytes[c]);
+        if (need_r)
+          for (int c = 0; c < a.nr; ++c) total += bytes(d.b_lo, d.b_hi, a.r_bytes[c]);
         for (int c = 0; c < a.ns; ++c) total += bytes(d.q_lo, d.q_hi, a.s_bytes[c]);
         if (pre) total += bytes(d.q_lo, d.q_hi, 2);
       }
@@ -697,10 +709,11 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
         dev::tma_load_1d(st + off, static_cast<const uint8_t*>(base) + dev::align_lo(lo, w) * w,
                          bytes(lo, hi, w), &full[b]);
       };
-      if (!pre) copy(a.off_bk, a.bkeys, d.b_lo, d.b_hi, kb);
+      if (need_keys) copy(a.off_bk, a.bkeys, d.b_lo, d.b_hi, kb);
       copy(a.off_pk, a.pkeys, d.q_lo, d.q_hi, kb);
       if (WRITE) {
-        for (int c = 0; c < a.nr; ++c) copy(a.off_r[c], a.r_src[c], d.b_lo, d.b_hi, a.r_bytes[c]);
+        if (need_r)
+          for (int c = 0; c < a.nr; ++c) copy(a.off_r[c], a.r_src[c], d.b_lo, d.b_hi, a.r_bytes[c]);
         for (int c = 0; c < a.ns; ++c) copy(a.off_s[c], a.s_src[c], d.q_lo, d.q_hi, a.s_bytes[c]);
         if (pre) copy(a.off_e, a.match_e, d.q_lo, d.q_hi, 2);
       }
