@@ -1168,7 +1168,11 @@ void lsd_partition_group(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t
 void lsd_partition(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, int key_bytes,
                    const PassPlan& plan, const ValCols& vals, std::vector<uint32_t>* counts_out,
                    unsigned long long* key_or) {
-  constexpr uint32_t kGroupBytes = 32;
+  // payload bytes per column group (CJ_GROUP_BYTES: experiments)
+  static const uint32_t kGroupBytes = [] {
+    const char* e = std::getenv("CJ_GROUP_BYTES");
+    return e ? (uint32_t)std::max(4, std::atoi(e)) : 32u;
+  }();
   uint32_t total = 0;
   for (int c = 0; c < vals.n; ++c) total += vals.bytes[c];
   if (total <= kGroupBytes)

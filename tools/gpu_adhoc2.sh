@@ -1,3 +1,2 @@
 cd $GRAFT_REPO_ROOT 2>/dev/null || cd /root/repo
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q > /tmp/t.log 2>&1; tail -1 /tmp/t.log
-for c in C2 C3 C4z1.5; do CONFIG=$c timeout 300 python tools/diag.py phj-gftr phj-gfur 2>&1 | grep " 3 wall"; done
+for g in 32 24 16 12; do echo "== group $g"; CJ_GROUP_BYTES=$g CONFIG=C3 timeout 300 python tools/diag.py phj-gftr smj-gftr 2>&1 | grep " 3 wall"; done
