@@ -198,6 +198,10 @@ void copy_columns(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, int
 // 9-bit digits, whichever needs fewer passes).
 PassPlan sort_plan(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes, const ValCols& vals);
 
+// Stable LSD over a plan of any length (segments of CJ_MAX_PASSES passes), engine.cu.
+void lsd_any(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, int kb,
+             const PassPlan& plan, const ValCols& vals, unsigned long long* key_or = nullptr);
+
 // ---- gather.cu ----------------------------------------------------------------
 void gather_cols(cj_ctx* ctx, const void* const* in, uint64_t n_in, const uint32_t* map,
                  uint64_t m, void* const* out, const uint32_t* bytes, int ncols);

@@ -178,7 +178,7 @@ void check_key_bytes(uint32_t kb) {
 // LSD plans longer than CJ_MAX_PASSES (e.g. 20 bits at 1 bit/pass) run in
 // segments; each segment is itself stable, so the composition is the plan.
 void lsd_any(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t n, int kb,
-             const PassPlan& plan, const ValCols& vals, unsigned long long* key_or = nullptr) {
+             const PassPlan& plan, const ValCols& vals, unsigned long long* key_or) {
   if (plan.npasses <= CJ_MAX_PASSES) {
     lsd_partition(ctx, keys, keys_out, n, kb, plan, vals, nullptr, key_or);
     return;

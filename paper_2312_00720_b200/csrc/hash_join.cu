@@ -176,6 +176,8 @@ struct FindArgs {
   // a duplicate build key sets *spec_fail, later units stop, and the caller
   // runs count + fill
   uint32_t* spec_fail;
+  uint32_t* spec_rows;  // probe rows of the units that matched completely (coverage check:
+                        // partitions without build rows have no units)
 };
 
 // Multiplicative (Fibonacci) hashing as the reference's ChunkTable
@@ -986,6 +988,7 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
         sync_c();
         continue;
       }
+      if (tid == 0) atomicAdd(a.spec_rows, nq);
     }
 
     // 3. emit finished rows in probe order at the unit's offset
@@ -1155,8 +1158,10 @@ uint64_t run_find(cj_ctx* ctx, FindArgs a, uint64_t total_units) {
       CJ_CUDA(cudaGetLastError());
       uint32_t* h = ctx->host_pinned;
       CJ_CUDA(cudaMemcpyAsync(h, a.spec_fail, 4, cudaMemcpyDeviceToHost, ctx->stream));
+      CJ_CUDA(cudaMemcpyAsync(h + 1, a.spec_rows, 4, cudaMemcpyDeviceToHost, ctx->stream));
       CJ_CUDA(cudaStreamSynchronize(ctx->stream));
-      if (h[0] == 0) return a.np_rows;  // every probe row matched once
+      // every unit matched completely AND the units covered every probe row
+      if (h[0] == 0 && h[1] == a.np_rows) return a.np_rows;
     }
     a.spec_fail = nullptr;
     if (U > 0) {
@@ -1305,8 +1310,10 @@ uint64_t phj_find(cj_ctx* ctx, const void* bkeys, const uint64_t* boff, const vo
   // speculate that every probe row finds its key (PK-FK): skips the count
   // pass when it holds (C2, C4); a miss falls back to count + fill
   const char* se = std::getenv("CJ_SPECULATE");
-  if (pk_fk && capacity >= out.s_rows && !(se && std::strcmp(se, "0") == 0))
+  if (pk_fk && capacity >= out.s_rows && !(se && std::strcmp(se, "0") == 0)) {
     a.spec_fail = ctx->ticket(3);
+    a.spec_rows = ctx->ticket(5);
+  }
   a.capacity = capacity;
   a.padded = out.padded ? 1 : 0;
   a.nb_rows = out.r_rows;

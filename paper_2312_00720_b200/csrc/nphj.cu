@@ -4,10 +4,12 @@
 // canonical row multiset, and the emission order is defined here as (probe
 // position, ascending build row).
 //
-// Slots are rows of 32-bit words: [row+1][key (1|2 words)][payload words...].
-// GFTR stores the build payload columns inside the slot (the hashed build
-// relation IS the transformed relation), so materialising a match reads the
-// key's own sector; GFUR stores only (row, key) and gathers payloads later.
+// Unique build keys (PK): slots are rows of 32-bit words [row+1][key (1|2
+// words)][payload words...]. GFTR stores the build payload columns inside the
+// slot (the hashed build relation IS the transformed relation), so
+// materialising a match reads the key's own sector; GFUR stores only (row,
+// key) and gathers payloads later.  Non-unique builds: the build is sorted
+// (stable, with row ids) and the table holds one slot per distinct key.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -50,6 +52,11 @@ struct NphjArgs {
   int write;
   uint64_t* total_out;
   int unique;                // build keys unique (Relation::key_unique): one match per probe
+  // non-unique builds: the build keys sorted (stable) with their row ids; the
+  // table holds one slot per distinct key [run start + 1][key], a probe finds
+  // its run's end by galloping over the sorted keys
+  const void* sorted_keys;
+  const uint32_t* sorted_ids;
 };
 
 template <class K>
@@ -229,14 +236,58 @@ __global__ void __launch_bounds__(kThreads) k_nphj_probe_u(const __grid_constant
   }
 }
 
+// Non-unique builds: one slot per distinct key of the sorted build (its run
+// start), so equal keys never form a probe chain (emission order unchanged:
+// probe position, then ascending build row).
 template <class K>
-__global__ void __launch_bounds__(kThreads) k_nphj_probe(const __grid_constant__ NphjArgs a) {
+__global__ void __launch_bounds__(kThreads) k_nphj_build_runs(const __grid_constant__ NphjArgs a) {
+  const K* __restrict__ sk = static_cast<const K*>(a.sorted_keys);
+  const uint64_t mask = (1ull << a.log2cap) - 1;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.nr;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const K k = sk[i];
+    if (i > 0 && sk[i - 1] == k) continue;
+    uint64_t h = nslot(k, a.log2cap);
+    while (true) {
+      uint32_t* sl = a.table + h * a.slot_words;
+      if (atomicCAS(sl, 0u, (uint32_t)(i + 1)) == 0u) {
+        sl[1] = (uint32_t)k;
+        if constexpr (sizeof(K) == 8) sl[2] = (uint32_t)((uint64_t)k >> 32);
+        break;
+      }
+      h = (h + 1) & mask;
+    }
+  }
+}
+
+// First index >= lo whose sorted key differs from k (galloping, then binary).
+template <class K>
+__device__ __forceinline__ uint64_t run_end(const K* __restrict__ sk, uint64_t n, uint64_t lo, K k) {
+  uint64_t step = 1, prev = lo;
+  uint64_t hi = lo + 1;
+  while (hi < n && sk[hi] == k) {
+    prev = hi;
+    step <<= 1;
+    hi = lo + step;
+  }
+  if (hi > n) hi = n;
+  uint64_t l = prev + 1;  // sk[prev] == k; answer in [l, hi]
+  while (l < hi) {
+    const uint64_t mid = (l + hi) >> 1;
+    if (sk[mid] == k) l = mid + 1; else hi = mid;
+  }
+  return l;
+}
+
+template <class K>
+__global__ void __launch_bounds__(kThreads) k_nphj_probe_runs(const __grid_constant__ NphjArgs a) {
   __shared__ uint32_t s_m[kTile];
   __shared__ uint64_t s_first[kTile];
   __shared__ uint64_t s_t, s_base;
   __shared__ uint64_t s_wcount[kWarps], s_wbase[kWarps];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const K* __restrict__ sk = static_cast<const K*>(a.skeys);
+  const K* __restrict__ bk = static_cast<const K*>(a.sorted_keys);
   const uint64_t mask = (1ull << a.log2cap) - 1;
   while (true) {
     if (tid == 0) s_t = atomicAdd(a.ticket, 1u);
@@ -256,12 +307,13 @@ __global__ void __launch_bounds__(kThreads) k_nphj_probe(const __grid_constant__
         uint32_t m = 0;
         uint64_t first = 0;
         while (true) {
-          const uint32_t* s = a.table + h * a.slot_words;
-          const uint32_t row1 = s[0];
+          const uint32_t* sl = a.table + h * a.slot_words;
+          const uint32_t row1 = sl[0];
           if (row1 == 0) break;
-          if (slot_key<K>(s) == k) {
-            if (m == 0) first = h;
-            ++m;
+          if (slot_key<K>(sl) == k) {
+            first = row1 - 1;
+            m = (uint32_t)(run_end<K>(bk, a.nr, first, k) - first);
+            break;
           }
           h = (h + 1) & mask;
         }
@@ -293,46 +345,26 @@ __global__ void __launch_bounds__(kThreads) k_nphj_probe(const __grid_constant__
         const uint32_t m = jl < nq ? s_m[jl] : 0;
         const uint32_t inc = dev::warp_inclusive_sum(m);
         const uint64_t obase = o + inc - m;
-        if (m) {
-          const uint64_t j = j0 + jl;
-          const K k = sk[j];
-          // matches in ascending build row: selection over the chain
-          uint64_t last_row = 0;  // rows are stored +1
-          for (uint32_t q = 0; q < m; ++q) {
-            uint64_t best = ~0ull, best_slot = 0;
-            uint64_t h = m == 1 ? s_first[jl] : nslot(k, a.log2cap);
-            while (true) {
-              const uint32_t* s = a.table + h * a.slot_words;
-              const uint32_t row1 = s[0];
-              if (row1 == 0) break;
-              if (slot_key<K>(s) == k && row1 > last_row && row1 < best) {
-                best = row1;
-                best_slot = h;
-                if (m == 1) break;
-              }
-              h = (h + 1) & mask;
-            }
-            last_row = best;
-            const uint64_t oo = obase + q;
-            if (oo >= a.capacity) continue;
-            const uint32_t* s = a.table + best_slot * a.slot_words;
-            const uint32_t i = (uint32_t)(best - 1);
-            if (a.key_out) static_cast<K*>(a.key_out)[oo] = k;
-            if (a.ids_r) a.ids_r[oo] = i;
-            if (a.ids_s) a.ids_s[oo] = (uint32_t)j;
-            for (int c = 0; c < a.nr_cols; ++c) {
-              const uint32_t* w = s + a.r_word_off[c];
-              if (a.r_bytes[c] == 4)
-                static_cast<uint32_t*>(a.r_dst[c])[oo] = w[0];
-              else
-                static_cast<uint64_t*>(a.r_dst[c])[oo] = (uint64_t)w[0] | ((uint64_t)w[1] << 32);
-            }
-            for (int c = 0; c < a.ns_cols; ++c) {
-              if (a.s_bytes[c] == 4)
-                static_cast<uint32_t*>(a.s_dst[c])[oo] = static_cast<const uint32_t*>(a.s_src[c])[j];
-              else
-                static_cast<uint64_t*>(a.s_dst[c])[oo] = static_cast<const uint64_t*>(a.s_src[c])[j];
-            }
+        const uint64_t j = j0 + jl;
+        // the run holds the matches in ascending build row (stable sort)
+        for (uint32_t q = 0; q < m; ++q) {
+          const uint64_t oo = obase + q;
+          if (oo >= a.capacity) break;
+          const uint32_t i = a.sorted_ids[s_first[jl] + q];
+          if (a.key_out) static_cast<K*>(a.key_out)[oo] = sk[j];
+          if (a.ids_r) a.ids_r[oo] = i;
+          if (a.ids_s) a.ids_s[oo] = (uint32_t)j;
+          for (int c = 0; c < a.nr_cols; ++c) {
+            if (a.r_bytes[c] == 4)
+              static_cast<uint32_t*>(a.r_dst[c])[oo] = static_cast<const uint32_t*>(a.r_src[c])[i];
+            else
+              static_cast<uint64_t*>(a.r_dst[c])[oo] = static_cast<const uint64_t*>(a.r_src[c])[i];
+          }
+          for (int c = 0; c < a.ns_cols; ++c) {
+            if (a.s_bytes[c] == 4)
+              static_cast<uint32_t*>(a.s_dst[c])[oo] = static_cast<const uint32_t*>(a.s_src[c])[j];
+            else
+              static_cast<uint64_t*>(a.s_dst[c])[oo] = static_cast<const uint64_t*>(a.s_src[c])[j];
           }
         }
         o += __shfl_sync(0xffffffffu, inc, 31);
@@ -342,12 +374,60 @@ __global__ void __launch_bounds__(kThreads) k_nphj_probe(const __grid_constant__
   }
 }
 
+// Non-unique builds: stable sort of the build keys with their row ids, one
+// table slot per distinct key, probes read whole runs (no equal-key chains:
+// a key repeated d times used to cost d^2 probe steps).
+template <class K>
+uint64_t run_sorted(cj_ctx* ctx, NphjArgs a) {
+  const uint64_t n = a.nr;
+  Scratch skeys(ctx, n * sizeof(K) + kPad), sids(ctx, n * 4 + kPad);
+  ValCols v;
+  v.n = 1;
+  v.gen_ids = 1;
+  v.bytes[0] = 4;
+  v.out[0] = sids.p;
+  lsd_any(ctx, a.rkeys, skeys.p, n, (int)sizeof(K), sort_plan(ctx, a.rkeys, n, sizeof(K), v), v,
+          nullptr);
+  a.sorted_keys = skeys.p;
+  a.sorted_ids = sids.as<uint32_t>();
+  a.slot_words = 1 + a.key_words;
+  const uint64_t cap = 1ull << a.log2cap;
+  Scratch table(ctx, cap * a.slot_words * 4);
+  CJ_CUDA(cudaMemsetAsync(table.p, 0, cap * a.slot_words * 4, ctx->stream));
+  a.table = table.as<uint32_t>();
+  Scratch tot(ctx, 8);
+  CJ_CUDA(cudaMemsetAsync(tot.p, 0, 8, ctx->stream));
+  a.total_out = tot.as<uint64_t>();
+  a.err = ctx->err_word;
+  ctx->kbegin("nphj_build", n * (uint64_t)(2 * sizeof(K) + 4ull * a.slot_words));
+  k_nphj_build_runs<K><<<grid_for(n, kThreads * 4, ctx->num_sms * 16), kThreads, 0, ctx->stream>>>(a);
+  ctx->kend();
+  a.tiles = (a.ns + kTile - 1) / kTile;
+  if (a.tiles > 0) {
+    a.status = ctx->status_buffer(a.tiles);
+    a.epoch = ctx->next_epoch();
+    a.ticket = ctx->ticket(3);
+    int per_sm = 0;
+    CJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_nphj_probe_runs<K>, kThreads, 0));
+    const uint64_t grid = std::min<uint64_t>((uint64_t)ctx->num_sms * std::max(per_sm, 1), a.tiles);
+    ctx->kbegin(a.write ? "nphj_probe" : "nphj_count", 0);
+    k_nphj_probe_runs<K><<<(unsigned)grid, kThreads, 0, ctx->stream>>>(a);
+    ctx->kend();
+  }
+  CJ_CUDA(cudaGetLastError());
+  uint64_t* h = reinterpret_cast<uint64_t*>(ctx->host_pinned);
+  CJ_CUDA(cudaMemcpyAsync(h, tot.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CJ_CUDA(cudaStreamSynchronize(ctx->stream));
+  return h[0];
+}
+
 template <class K>
 uint64_t run(cj_ctx* ctx, NphjArgs a) {
   uint32_t log2cap = 1;
   while ((1ull << log2cap) < 2 * std::max<uint64_t>(a.nr, 1)) ++log2cap;
   a.log2cap = log2cap;
   a.key_words = sizeof(K) / 4;
+  if (!a.unique && a.nr > 0) return run_sorted<K>(ctx, a);
   uint32_t words = 1 + a.key_words;
   for (int c = 0; c < a.nr_cols; ++c) {
     a.r_word_off[c] = words;
@@ -383,13 +463,10 @@ uint64_t run(cj_ctx* ctx, NphjArgs a) {
       kern<<<(unsigned)grid, kThreads, 0, ctx->stream>>>(a);
       ctx->kend();
     };
+    // (non-unique builds took run_sorted above)
     const bool vec = sizeof(K) == 4 && a.slot_words == 4;
-    if (a.unique) {
-      if (vec) launch(k_nphj_probe_u<K, true>);
-      else launch(k_nphj_probe_u<K, false>);
-    } else {
-      launch(k_nphj_probe<K>);
-    }
+    if (vec) launch(k_nphj_probe_u<K, true>);
+    else launch(k_nphj_probe_u<K, false>);
   }
   CJ_CUDA(cudaGetLastError());
   uint64_t* h = reinterpret_cast<uint64_t*>(ctx->host_pinned);

@@ -1253,7 +1253,10 @@ void lsd_partition_group(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t
       off += col_span(c);
     }
   }
-  Scratch cnt2(ctx, live.size() > 1 ? sizeof(uint32_t) * kRadix * g0.nblocks + 4096 : 0);
+  // later passes may tile differently (the first pass generates GFUR ids
+  // instead of staging them): size for the most blocks any geometry uses
+  const uint64_t max_blocks = (uint64_t)ctx->num_sms * 2;
+  Scratch cnt2(ctx, live.size() > 1 ? sizeof(uint32_t) * kRadix * max_blocks + 4096 : 0);
   const void* cur_k = keys;
   ValCols cur = vals;
   bool to_out = (live.size() % 2) == 1;
@@ -1278,8 +1281,7 @@ void lsd_partition_group(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t
         one.npasses = 1;
         one.lo[0] = plan.lo[p];
         one.hi[0] = plan.hi[p];
-        if ((size_t)g.nblocks * kRadix * 4 > (size_t)kRadix * g0.nblocks * 4 + 4096)
-          fail(CJ_ERR_CUDA, "block count scratch too small");
+        if ((uint64_t)g.nblocks > max_blocks) fail(CJ_ERR_CUDA, "block count scratch too small");
         block_hist(ctx, cur_k, n, key_bytes, one, g, cnt2.as<uint32_t>());
         pc = cnt2.as<uint32_t>();
       }
