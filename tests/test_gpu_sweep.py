@@ -97,3 +97,51 @@ def test_random_case_matches_oracle(ctx, comm, i):
            [np.asarray(p).astype(np.uint64) for p in ref["payloads"]]
     assert out.matches == len(ref["key"]), (c, "sharded", algo, pattern)
     assert O.canonical_digest(got) == O.canonical_digest(want), (c, "sharded", algo, pattern)
+
+
+@pytest.mark.parametrize("i", range(60))
+def test_random_primitive_matches_oracle(ctx, i):
+    """Seeded random primitives: one-pass radix partitions, LSD partitions and
+    full sorts over random key widths, digit ranges, key distributions (wide,
+    narrow, duplicate-heavy, skewed, runs), sizes and value columns — bit-exact
+    keys, values and layouts against the oracle."""
+    g = np.random.default_rng(5000 + i)
+    kb = int(g.choice([4, 8]))
+    n = int(g.choice([0, 1, 31, 5000, 65536, 200003]))
+    dist = str(g.choice(["wide", "narrow", "dups", "zipf", "runs"]))
+    if dist == "wide":
+        k = g.integers(0, 2 ** 63, n, dtype=np.uint64)
+    elif dist == "narrow":
+        k = g.integers(0, 1 << int(g.integers(1, 20)), n, dtype=np.uint64)
+    elif dist == "dups":
+        k = g.integers(0, 17, n, dtype=np.uint64) * np.uint64(1 << 20)
+    elif dist == "zipf":
+        k = np.minimum(g.zipf(1.3, n), 1 << 30).astype(np.uint64)
+    else:
+        k = np.repeat(g.integers(0, 1 << 24, max(n // 500, 1), dtype=np.uint64), 500)[:n]
+        if k.size < n:
+            k = np.concatenate([k, np.zeros(n - k.size, np.uint64)])
+    k = k.astype(np.uint32 if kb == 4 else np.uint64)
+    vals = [g.integers(0, 2 ** 32, n, dtype=np.uint64).astype(np.uint32)
+            for _ in range(int(g.integers(0, 3)))]
+    vals += [g.integers(0, 2 ** 63, n, dtype=np.uint64) for _ in range(int(g.integers(0, 2)))]
+    dk, dv = cj.to_device(k), [cj.to_device(v) for v in vals]
+    op = str(g.choice(["partition", "passes", "sort"]))
+    if op == "partition":
+        lo = int(g.integers(0, 8 * kb - 1))
+        hi = min(8 * kb, lo + int(g.integers(1, 9)))
+        ko, vo, off = cj.radix_partition(ctx, dk, dv, lo, hi)
+        ek, ev, eoff = O.radix_partition(k, vals, lo, hi, key_bytes=kb)
+        assert np.array_equal(off, eoff[: off.size]), (i, op, lo, hi)
+    elif op == "passes":
+        bits = int(g.integers(0, 21))
+        per = int(g.integers(1, 9))
+        ko, vo, off = cj.partition_relation(ctx, dk, dv, bits, per)
+        ek, ev, eoff = O.partition_relation(k, vals, bits, per, key_bytes=kb)
+        assert np.array_equal(cj.to_host(off).astype(np.uint64), eoff), (i, op, bits, per)
+    else:
+        ko, vo = cj.sort_pairs(ctx, dk, dv)
+        ek, ev = O.sort_pairs(k, vals, key_bytes=kb)
+    assert np.array_equal(H(ko), np.asarray(ek).astype(np.uint64)), (i, op, dist, kb, n)
+    for a_, b_ in zip(vo, ev):
+        assert np.array_equal(H(a_), np.asarray(b_).astype(np.uint64)), (i, op, dist, kb, n)
