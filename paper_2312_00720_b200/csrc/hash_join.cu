@@ -569,8 +569,8 @@ __device__ __forceinline__ void emit_compact(const FindArgs& a, const UnitDesc& 
 // and hand them back per warp (empty barriers).  Units the count pass fully
 // resolved (the PK-FK fill) need no consumer-wide barrier at all; the other
 // paths synchronise the consumers on named barrier 1.
-template <class K, bool WRITE>
-__global__ void __launch_bounds__(kTmaThreads + 32, WRITE ? 1 : 2)
+template <class K, bool WRITE, int MINB>
+__global__ void __launch_bounds__(kTmaThreads + 32, MINB)
 k_phj_tma(const __grid_constant__ FindArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint32_t* tab = reinterpret_cast<uint32_t*>(smem + (size_t)a.stages * a.stage_bytes);
@@ -1093,7 +1093,8 @@ bool tma_layout(FindArgs& a, size_t* smem_out) {
   const size_t smem = (size_t)a.stages * off + up(4 * (size_t)a.cap_entries) +
                       (a.write ? (size_t)a.qchunk * 8 : 0);
   *smem_out = smem;
-  return smem <= 225 * 1024;  // + < 2 KB of static shared memory
+  // + < 2 KB of static shared memory per CTA
+  return smem <= (size_t)(a.write ? 225 / find_ctas_per_sm() - 2 : 225) * 1024;
 }
 
 // Probe rows per work unit: the largest (<= 8192, multiple of 128) whose two
@@ -1109,6 +1110,21 @@ uint32_t choose_qchunk(FindArgs a) {
     if (tma_layout<K>(a, &smem)) return q;
   }
   return probe_chunk();
+}
+
+// The fill at one CTA per SM (default), or two (CJ_FIND_CTAS=2: half the
+// shared memory each, probe chunks sized to fit, <= 60 registers).
+template <class K>
+void launch_fill(cj_ctx* ctx, const FindArgs& a, unsigned grid, size_t smem) {
+  if (find_ctas_per_sm() >= 2) {
+    CJ_CUDA(cudaFuncSetAttribute(k_phj_tma<K, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    k_phj_tma<K, true, 2><<<grid, kTmaThreads + 32, smem, ctx->stream>>>(a);
+  } else {
+    CJ_CUDA(cudaFuncSetAttribute(k_phj_tma<K, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    k_phj_tma<K, true, 1><<<grid, kTmaThreads + 32, smem, ctx->stream>>>(a);
+  }
 }
 
 template <class K>
@@ -1150,10 +1166,8 @@ uint64_t run_find(cj_ctx* ctx, FindArgs a, uint64_t total_units) {
       tma_layout<K>(as, &smem_s);
       const unsigned grid =
           (unsigned)std::min<uint64_t>((uint64_t)ctx->num_sms * find_ctas_per_sm(), U);
-      CJ_CUDA(cudaFuncSetAttribute(k_phj_tma<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem_s));
       ctx->kbegin("phj_find", 0);
-      k_phj_tma<K, true><<<grid, kTmaThreads + 32, smem_s, ctx->stream>>>(as);
+      launch_fill<K>(ctx, as, grid, smem_s);
       ctx->kend();
       CJ_CUDA(cudaGetLastError());
       uint32_t* h = ctx->host_pinned;
@@ -1178,10 +1192,10 @@ uint64_t run_find(cj_ctx* ctx, FindArgs a, uint64_t total_units) {
           (uint64_t)ctx->num_sms * (ec ? std::max(1, std::atoi(ec)) : 2), U);
       const unsigned grid =
           (unsigned)std::min<uint64_t>((uint64_t)ctx->num_sms * find_ctas_per_sm(), U);
-      CJ_CUDA(cudaFuncSetAttribute(k_phj_tma<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      CJ_CUDA(cudaFuncSetAttribute(k_phj_tma<K, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem_c));
       ctx->kbegin("phj_count", (uint64_t)(sizeof(K)) * (a.nb_rows + a.np_rows));
-      k_phj_tma<K, false><<<grid_c, kTmaThreads + 32, smem_c, ctx->stream>>>(ac);
+      k_phj_tma<K, false, 2><<<grid_c, kTmaThreads + 32, smem_c, ctx->stream>>>(ac);
       ctx->kend();
       scan_counts(ctx, counts.as<uint64_t>(), U, offs.as<uint64_t>(), a.total_out);
       CJ_CUDA(cudaGetLastError());
@@ -1192,10 +1206,8 @@ uint64_t run_find(cj_ctx* ctx, FindArgs a, uint64_t total_units) {
         a.unit_off = offs.as<uint64_t>();
         a.unit_counts = std::getenv("CJ_FIND_FAST") && std::strcmp(std::getenv("CJ_FIND_FAST"), "0") == 0
                             ? nullptr : counts.as<uint64_t>();
-        CJ_CUDA(cudaFuncSetAttribute(k_phj_tma<K, true>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tma_smem));
         ctx->kbegin("phj_find", 0);
-        k_phj_tma<K, true><<<grid, kTmaThreads + 32, tma_smem, ctx->stream>>>(a);
+        launch_fill<K>(ctx, a, grid, tma_smem);
         ctx->kend();
         CJ_CUDA(cudaGetLastError());
       }
