@@ -93,6 +93,9 @@ struct cj_ctx {
   // run_join's transforms: run every LSD pass without the constant-digit host
   // round trip (a constant pass is a stable copy; skipping it only saves time)
   bool assume_live_passes = false;
+  // set by a caller that synchronised and read a zero error word: the next
+  // raise_device_errors returns without another round trip
+  bool err_known_clean = false;
 };
 
 namespace cj {

@@ -58,6 +58,11 @@ void scan_counts(cj_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* out, uin
 }
 
 void raise_device_errors(cj_ctx* ctx) {
+  if (ctx->err_known_clean) {  // the caller just read the error word after a sync
+    ctx->err_known_clean = false;
+    CJ_CUDA(cudaStreamSynchronize(ctx->stream));  // callers rely on an idle stream after this
+    return;
+  }
   CJ_CUDA(cudaMemcpyAsync(ctx->host_pinned + 64, ctx->err_word, sizeof(uint32_t),
                           cudaMemcpyDeviceToHost, ctx->stream));
   CJ_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -598,8 +603,7 @@ void run_join_dev(cj_ctx* ctx, const cj_relation* R, const cj_relation* S,
   res->peak_materialize_b = peaks.next();
   res->device_bytes_peak =
       std::max({res->peak_transform_b, res->peak_find_b, res->peak_materialize_b});
-  CJ_CUDA(cudaStreamSynchronize(ctx->stream));
-  raise_device_errors(ctx);
+  raise_device_errors(ctx);  // (one synchronisation: it reads the error word)
   res->rows = total;
   res->transform_ns = tm.ns(0, 1);
   res->find_ns = tm.ns(1, 2);

@@ -1173,9 +1173,13 @@ uint64_t run_find(cj_ctx* ctx, FindArgs a, uint64_t total_units) {
       uint32_t* h = ctx->host_pinned;
       CJ_CUDA(cudaMemcpyAsync(h, a.spec_fail, 4, cudaMemcpyDeviceToHost, ctx->stream));
       CJ_CUDA(cudaMemcpyAsync(h + 1, a.spec_rows, 4, cudaMemcpyDeviceToHost, ctx->stream));
+      CJ_CUDA(cudaMemcpyAsync(h + 2, ctx->err_word, 4, cudaMemcpyDeviceToHost, ctx->stream));
       CJ_CUDA(cudaStreamSynchronize(ctx->stream));
       // every unit matched completely AND the units covered every probe row
-      if (h[0] == 0 && h[1] == a.np_rows) return a.np_rows;
+      if (h[0] == 0 && h[1] == a.np_rows) {
+        ctx->err_known_clean = h[2] == 0;
+        return a.np_rows;
+      }
     }
     a.spec_fail = nullptr;
     if (U > 0) {
