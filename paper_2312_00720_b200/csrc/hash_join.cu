@@ -761,6 +761,10 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
     const uint32_t rounds = (nq + 31) / 32;
     const uint32_t r0 = (uint32_t)((uint64_t)rounds * warp / kTmaWarps);
     const uint32_t r1 = (uint32_t)((uint64_t)rounds * (warp + 1) / kTmaWarps);
+    // the speculative fill alternates its probe results between res and the
+    // list region by unit parity, so a unit needs no barrier at its end
+    const bool spec = WRITE && a.spec_fail != nullptr;
+    uint32_t* const rs = spec ? res + (k & 1u) * a.qchunk : res;
     if (pre) {
       // matches resolved by the count pass
       const uint16_t* me = reinterpret_cast<const uint16_t*>(st + a.off_e) +
@@ -797,6 +801,10 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
     const uint32_t cap = 1u << cap_log2, cmask = cap - 1;
     // dense keys: slot = key >> dense_shift < cap for every build key
     const bool dense = key_hi < cap;
+    // A tagged direct-addressed table needs no clear and so no barrier before
+    // the inserts: every consumer passed the previous unit's post-probe
+    // barrier before reaching this point, so nobody still reads the table.
+    bool cleared = false;
     if (!reuse) {
       if (tid == 0) s_dup = 0;
       if (dense) {
@@ -804,14 +812,16 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
           for (uint32_t i = tid; i < a.cap_entries; i += kTmaThreads) tab[i] = 0;
           utag = 0;
           tab_tagged = true;
+          cleared = true;
         }
         ++utag;
       } else {
         for (uint32_t i = tid; i < cap; i += kTmaThreads) tab[i] = kNoMatch;
         tab_tagged = false;
+        cleared = true;
       }
     }
-    sync_c();
+    if (cleared) sync_c();
 
     // 1. insert chunk positions (CAS); meeting an equal key marks duplicates
     //    (a plain-store first round measured slower: profiles/r01b_summary.md).
@@ -824,8 +834,11 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
         for (uint32_t i = tid; i < nb; i += kTmaThreads) tab[(uint32_t)(bk[i] >> ds)] = tagged | i;
         sync_c();
         // equal keys share a slot: one of them does not find itself there
-        for (uint32_t i = tid; i < nb; i += kTmaThreads)
-          if (tab[(uint32_t)(bk[i] >> ds)] != (tagged | i)) dup = true;
+        // (the speculative fill checks this after its probe: a duplicate
+        // fails the unit either way)
+        if (!spec)
+          for (uint32_t i = tid; i < nb; i += kTmaThreads)
+            if (tab[(uint32_t)(bk[i] >> ds)] != (tagged | i)) dup = true;
       }
     } else {
       for (uint32_t i = reuse ? nb : tid; i < nb; i += kTmaThreads) {
@@ -839,9 +852,15 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
         }
       }
     }
-    if (dev::named_bar_or(1, kTmaThreads, dup)) s_dup = 1;
-    sync_c();
-    const bool has_dup = s_dup != 0;
+    // the OR-barrier also orders the inserts before the probes; a reused
+    // table's flag was stored by the unit that built it
+    const bool late_verify = spec && dense;
+    bool any_dup = false;
+    if (!late_verify) {
+      any_dup = dev::named_bar_or(1, kTmaThreads, dup);
+      if (any_dup && tid == 0) s_dup = 1;
+    }
+    const bool has_dup = reuse ? s_dup != 0 : any_dup;
     // a probe row of a split partition meets several build chunks, one unit
     // each, and matches in at most one: its match index cannot be handed to
     // the fill (the fill rebuilds those units' tables)
@@ -887,7 +906,7 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
         const uint32_t e = hi < cap ? tab[(uint32_t)hi] : 0u;
         const uint32_t m = (e >> 16) == utag;
         const uint32_t out = m ? (e & 0xffffu) : kNoMatch;
-        if (WRITE) res[jl] = out;
+        if (WRITE) rs[jl] = out;
         else if (me_out) me_out[jl] = (uint16_t)(m ? out : kEmpty16);
         wcount += m;
       }
@@ -928,7 +947,7 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
             ee = tab[ss];
             if (ee != kNoMatch) bb = bk[ee];
           }
-          if (WRITE) res[jl] = out;
+          if (WRITE) rs[jl] = out;
           else if (me_out) me_out[jl] = (uint16_t)(out == kNoMatch ? kEmpty16 : out);
           wcount += m;
         }
@@ -961,10 +980,30 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
           m = lo2 - lo;
           out = (lo << 16) | m;
         }
-        if (WRITE) res[jl] = out;
+        if (WRITE) rs[jl] = out;
         else if (me_out && !has_dup) me_out[jl] = (uint16_t)(out == kNoMatch ? kEmpty16 : out);
         wcount += m;
       }
+    }
+    if (WRITE && a.spec_fail) {
+      // speculation: this unit's rows go to its probe offset only if every
+      // probe row matched exactly once — one OR-barrier over "a row of mine
+      // missed" replaces the count, its barrier and the scan (the output rows
+      // are then the probe rows in order)
+      const uint32_t full = nq >> 5, rem = nq & 31;
+      uint32_t mine = r0 < min(r1, full) ? min(r1, full) - r0 : 0u;
+      if (full >= r0 && full < r1 && (uint32_t)lane < rem) ++mine;
+      if (late_verify && !reuse)
+        for (uint32_t i = tid; i < nb; i += kTmaThreads)
+          if (tab[(uint32_t)(bk[i] >> ds)] != (tagged | i)) dup = true;
+      if (dev::named_bar_or(1, kTmaThreads, has_dup || dup || wcount != mine)) {
+        if (tid == 0) atomicExch(a.spec_fail, 1u);
+      } else {
+        if (tid == 0) atomicAdd(a.spec_rows, nq);
+        emit_rows<K>(a, inf, st, pk, nullptr, rs, nullptr, s_ubase[b], nq, true);
+      }
+      release(b);
+      continue;
     }
     wcount = (uint32_t)dev::warp_sum((uint64_t)wcount);
     if (lane == 0) s_wcount[warp] = wcount;
@@ -978,19 +1017,6 @@ k_phj_tma(const __grid_constant__ FindArgs a) {
     }
     if (!WRITE) continue;
     sync_c();
-    if (a.spec_fail) {
-      // speculation: this unit's rows go to its probe offset only if every
-      // probe row matched exactly once
-      const uint64_t got = s_wbase[kTmaWarps - 1] + s_wcount[kTmaWarps - 1] - s_ubase[b];
-      if (has_dup || got != nq) {
-        if (tid == 0) atomicExch(a.spec_fail, 1u);
-        release(b);
-        sync_c();
-        continue;
-      }
-      if (tid == 0) atomicAdd(a.spec_rows, nq);
-    }
-
     // 3. emit finished rows in probe order at the unit's offset
     const uint32_t bsh4 = (uint32_t)(inf.b_lo & 3), bsh8 = (uint32_t)(inf.b_lo & 1);
     const uint32_t qsh4 = (uint32_t)(inf.q_lo & 3), qsh8 = (uint32_t)(inf.q_lo & 1);
