@@ -73,6 +73,11 @@ struct SmjArgs {
   uint8_t* tile_pre;
   uint32_t off_e;
   int nstages;               // TMA stage ring depth (2..kSmjMaxStages)
+  // speculative PK-FK fill (no count pass): every probe row is expected to
+  // find its key, so tile t writes its rows at its first probe row; a tile
+  // with a miss sets *spec_fail and the caller runs count + fill
+  uint32_t* spec_fail;
+  uint32_t* spec_rows;       // probe rows of the tiles that matched completely
 };
 
 template <class K>
@@ -242,7 +247,8 @@ struct SmjDesc {
 template <class K>
 __global__ void k_smj_bounds(const K* __restrict__ r, uint64_t nr, const K* __restrict__ s,
                              uint64_t ns, uint64_t tiles, SmjDesc* __restrict__ desc,
-                             uint64_t wide_lim, uint32_t* __restrict__ wide) {
+                             uint64_t wide_lim, uint32_t* __restrict__ wide,
+                             uint32_t* __restrict__ miss) {
   for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < tiles;
        t += (uint64_t)gridDim.x * blockDim.x) {
     SmjDesc d;
@@ -252,6 +258,10 @@ __global__ void k_smj_bounds(const K* __restrict__ r, uint64_t nr, const K* __re
     d.r_hi = g_upper_bound<K>(r, d.r_lo, nr, s[d.s_hi - 1]);
     desc[t] = d;
     if (wide && d.r_hi - d.r_lo > wide_lim) atomicAdd(wide, 1u);
+    // a tile's first or last probe key absent from r: not every probe matches
+    // (the PK-FK speculation would fail; it is not tried)
+    if (miss && (d.r_hi == d.r_lo || r[d.r_lo] != s[d.s_lo] || r[d.r_hi - 1] != s[d.s_hi - 1]))
+      atomicOr(miss, 1u);
   }
 }
 
@@ -365,6 +375,7 @@ __global__ void __launch_bounds__(kTmaThreads + 32, 1) k_smj_tma(const __grid_co
   __shared__ SmjDesc s_desc[kSmjMaxStages];
   __shared__ bool s_pre[kSmjMaxStages];
   __shared__ uint64_t s_fcnt[kSmjMaxStages], s_fbase[kSmjMaxStages];
+  __shared__ int s_abort[kSmjMaxStages];  // speculative fill: the producer stopped at this stage
   __shared__ __align__(8) uint64_t full[kSmjMaxStages], empty[kSmjMaxStages];
   __shared__ uint64_t s_wcnt[2][kTmaWarps], s_wb[2][kTmaWarps];  // by tile parity
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -417,6 +428,13 @@ __global__ void __launch_bounds__(kTmaThreads + 32, 1) k_smj_tma(const __grid_co
         pr ^= 1u;
       }
       const SmjDesc d = cur.d;
+      if (WRITE && a.spec_fail && *reinterpret_cast<volatile uint32_t*>(a.spec_fail)) {
+        // a tile failed the speculation: wake the consumers on this stage and stop
+        s_abort[b] = 1;
+        dev::mbar_arrive(&full[b]);
+        return;
+      }
+      s_abort[b] = 0;
       const bool pre = cur.pre != 0;
       s_desc[b] = d;
       s_pre[b] = pre;
@@ -474,9 +492,13 @@ __global__ void __launch_bounds__(kTmaThreads + 32, 1) k_smj_tma(const __grid_co
     uint64_t* s_wbase = s_wb[par];
     dev::mbar_wait(&full[b], cphase);
     const SmjDesc d = s_desc[b];
+    if (WRITE && s_abort[b]) break;  // the speculation failed: the producer stopped
     const bool pre = s_pre[b];
+    // the speculative fill alternates its lower bounds between loff and the
+    // list region by tile parity, so a tile needs no barrier at its end
+    uint32_t* const lw = WRITE && a.spec_fail && par ? list : loff;
     uint64_t tile_base = 0;
-    if (WRITE && tid == 32) tile_base = a.tile_off[t];
+    if (WRITE && tid == 32) tile_base = a.spec_fail ? d.s_lo : a.tile_off[t];
     uint8_t* st = smem + (size_t)b * a.stage_bytes;
     const uint32_t nq = (uint32_t)(d.s_hi - d.s_lo);
     const uint64_t w = d.r_hi - d.r_lo;
@@ -507,7 +529,7 @@ __global__ void __launch_bounds__(kTmaThreads + 32, 1) k_smj_tma(const __grid_co
       for (uint32_t q = 0; q < kSmjPer; ++q) {
         const uint32_t jl = j0 + q;
         const uint32_t e = jl < nq ? me[jl] : 0xffffu;
-        loff[jl] = e;
+        lw[jl] = e;
         mcnt[jl] = e != 0xffffu;
         tsum += e != 0xffffu;
       }
@@ -536,7 +558,7 @@ __global__ void __launch_bounds__(kTmaThreads + 32, 1) k_smj_tma(const __grid_co
           const bool hit = inr && rk[i] == k && (i == 0 || rk[i - 1] < k);
           if (hit || !inr) {
             lb = k < rlo ? 0u : (hit ? i : (uint32_t)w);
-            loff[jl] = lb;
+            lw[jl] = lb;
             mcnt[jl] = hit;
             tsum += hit;
             e16[q] = hit ? (uint16_t)lb : (uint16_t)0xffffu;
@@ -568,7 +590,7 @@ __global__ void __launch_bounds__(kTmaThreads + 32, 1) k_smj_tma(const __grid_co
           }
           uint32_t m = 0;
           if (lb < w && rk[lb] == k) m = a.pk_fk ? 1u : gallop<K, true>(rk, lb, (uint32_t)w, k) - lb;
-          loff[jl] = lb;
+          lw[jl] = lb;
           mcnt[jl] = m;
           tsum += m;
           e16[q] = (uint16_t)(m ? lb : 0xffffu);
@@ -590,13 +612,33 @@ __global__ void __launch_bounds__(kTmaThreads + 32, 1) k_smj_tma(const __grid_co
           const uint64_t g = g_lower_bound<K>(rg, d.r_lo, d.r_hi, k);
           uint64_t m = 0;
           if (g < d.r_hi && rg[g] == k) m = a.pk_fk ? 1 : g_upper_bound<K>(rg, g, d.r_hi, k) - g;
-          loff[jl] = (uint32_t)(g - d.r_lo);
+          lw[jl] = (uint32_t)(g - d.r_lo);
           mcnt[jl] = (uint32_t)m;
           tsum += (uint32_t)m;
         }
       }
     }
     if (!WRITE && a.match_e && tid == 0) a.tile_pre[t] = (a.pk_fk && win) ? 1 : 0;
+    if (WRITE && a.spec_fail) {
+      // speculation: unique build keys match a probe at most once, so the tile
+      // holds iff no thread saw a miss among its probes — one OR-barrier, no
+      // count or scan; the output rows are then the probe rows in order
+      uint32_t mine = 0;
+#pragma unroll
+      for (uint32_t q = 0; q < kSmjPer; ++q) mine += j0 + q < nq ? 1u : 0u;
+      if (dev::named_bar_or(1, kTmaThreads, tsum != mine)) {
+        if (tid == 0) atomicExch(a.spec_fail, 1u);
+        release(b);
+        continue;  // loff / mcnt are not read again
+      }
+      if (tid == 0) atomicAdd(a.spec_rows, nq);
+      if (win) {
+        smj_emit_rows<K>(a, d, st, sk, d.s_lo, nq, [&](uint32_t tt) { return (lw[tt] << 16) | tt; });
+        release(b);
+        continue;
+      }
+      // a window beyond shared memory: the general emission below, at d.s_lo
+    }
     const uint32_t tinc = dev::warp_inclusive_sum(tsum);
     if (lane == 31) s_wcount[warp] = tinc;
     consumers_sync();
@@ -624,7 +666,7 @@ __global__ void __launch_bounds__(kTmaThreads + 32, 1) k_smj_tma(const __grid_co
         for (uint32_t q = 0; q < kSmjPer; ++q) {
           const uint32_t jl = j0 + q;
           if (jl < nq) {
-            const uint32_t m = mcnt[jl], l0 = loff[jl];
+            const uint32_t m = mcnt[jl], l0 = lw[jl];
             for (uint32_t i = 0; i < m; ++i) list[o++] = ((l0 + i) << 16) | jl;
           }
         }
@@ -632,7 +674,7 @@ __global__ void __launch_bounds__(kTmaThreads + 32, 1) k_smj_tma(const __grid_co
       }
       // 2b. column by column, consecutive threads on consecutive output rows
       const uint32_t* lst = list;
-      const uint32_t* lof = loff;
+      const uint32_t* lof = lw;
       if (ident)
         smj_emit_rows<K>(a, d, st, sk, tbase, (uint32_t)tcount,
                          [&](uint32_t tt) { return (lof[tt] << 16) | tt; });
@@ -655,7 +697,7 @@ __global__ void __launch_bounds__(kTmaThreads + 32, 1) k_smj_tma(const __grid_co
       if (m) {
         const uint64_t j = d.s_lo + jl;
         const K k = sk[jl];
-        const uint32_t l0 = loff[jl];
+        const uint32_t l0 = lw[jl];
         for (uint32_t q = 0; q < m; ++q, ++oo) {
           if (oo >= a.capacity) continue;
           const uint32_t li = l0 + q;
@@ -771,15 +813,51 @@ uint64_t run_tma(cj_ctx* ctx, SmjArgs a) {
   // tiles whose r window needs the 4096-key stages (skewed or sparse probes):
   // the fill takes three stages only when they are rare
   uint32_t* wide = ctx->ticket(4);
+  uint32_t* miss = ctx->ticket(8);
   k_smj_bounds<K><<<grid_for(a.tiles, 128, 4096), 128, 0, ctx->stream>>>(
       static_cast<const K*>(a.r), a.nr, static_cast<const K*>(a.s), a.ns, a.tiles,
-      desc.as<SmjDesc>(), 2048, a.write ? wide : nullptr);
+      desc.as<SmjDesc>(), 2048, a.write ? wide : nullptr, a.write && a.pk_fk ? miss : nullptr);
   ctx->kend();
   int fill_stages = 2;
+  bool boundary_miss = true;
   if (a.write) {
     CJ_CUDA(cudaMemcpyAsync(ctx->host_pinned, wide, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CJ_CUDA(cudaMemcpyAsync(ctx->host_pinned + 1, miss, 4, cudaMemcpyDeviceToHost, ctx->stream));
     CJ_CUDA(cudaStreamSynchronize(ctx->stream));
     fill_stages = (uint64_t)ctx->host_pinned[0] * 64 <= a.tiles ? 3 : 2;
+    boundary_miss = ctx->host_pinned[1] != 0;
+  }
+  // PK-FK speculation: one fill pass, each tile at its first probe row; a miss
+  // anywhere falls back to count + fill below (CJ_SPECULATE=0: off)
+  const char* se = std::getenv("CJ_SPECULATE");
+  if (a.write && a.pk_fk && !boundary_miss && a.capacity >= a.ns &&
+      !(se && std::strcmp(se, "0") == 0)) {
+    SmjArgs as = a;
+    as.match_e = nullptr;
+    as.tile_pre = nullptr;
+    as.tile_counts = nullptr;
+    as.tile_off = nullptr;
+    as.spec_fail = ctx->ticket(6);
+    as.spec_rows = ctx->ticket(7);
+    const size_t smem_s = smj_layout<K>(as, true, fill_stages);
+    if (smem_s <= 220 * 1024) {
+      CJ_CUDA(cudaFuncSetAttribute(k_smj_tma<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem_s));
+      const unsigned grid_s = (unsigned)std::min<uint64_t>((uint64_t)ctx->num_sms, a.tiles);
+      ctx->kbegin("smj_find", 0);
+      k_smj_tma<K, true><<<grid_s, kTmaThreads + 32, smem_s, ctx->stream>>>(as);
+      ctx->kend();
+      CJ_CUDA(cudaGetLastError());
+      uint32_t* h = ctx->host_pinned;
+      CJ_CUDA(cudaMemcpyAsync(h, as.spec_fail, 4, cudaMemcpyDeviceToHost, ctx->stream));
+      CJ_CUDA(cudaMemcpyAsync(h + 1, as.spec_rows, 4, cudaMemcpyDeviceToHost, ctx->stream));
+      CJ_CUDA(cudaMemcpyAsync(h + 2, ctx->err_word, 4, cudaMemcpyDeviceToHost, ctx->stream));
+      CJ_CUDA(cudaStreamSynchronize(ctx->stream));
+      if (h[0] == 0 && h[1] == a.ns) {
+        ctx->err_known_clean = h[2] == 0;
+        return a.ns;
+      }
+    }
   }
   SmjArgs ac = a;
   ac.tile_counts = counts.as<uint64_t>();

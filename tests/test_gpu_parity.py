@@ -424,6 +424,28 @@ def test_smj_mislabelled_unique_build(ctx, kb):
     _smj_case(ctx, rk, sk, True, seed=kb)
 
 
+@pytest.mark.parametrize("kb", [4, 8])
+@pytest.mark.parametrize("miss", ["none", "interior", "last"])
+def test_pk_fk_speculation_misses(ctx, kb, miss):
+    """PK-FK joins whose probe keys all match but for one key inside a merge
+    tile (its first and last keys still match, so SMJ's tile-boundary check
+    lets the speculative fill run and fail), or the largest probe key: the
+    speculative one-pass fills (PHJ units, SMJ tiles) must fall back to count +
+    fill and give the reference's rows in order."""
+    n = 1 << 16
+    g = np.random.default_rng(7 + kb)
+    dt = np.uint32 if kb == 4 else np.uint64
+    rk = (2 * g.permutation(n)).astype(dt)                  # unique even keys
+    sk = np.repeat(np.arange(n, dtype=np.uint64) * 2, 2)    # every key twice
+    if miss == "interior":
+        sk[1001] = 1001  # sorted position ~1001 of a 2048-row tile: odd, absent
+    elif miss == "last":
+        sk[-1] = 2 * n + 1
+    sk = sk.astype(dt)
+    g.shuffle(sk)
+    _smj_case(ctx, rk, sk, True, seed=kb)
+
+
 # ---- MemLedger view of the device arena (mem_ledger.hpp:26-100) --------------
 def dev_rel(X, uniq):
     return cj.Relation(cj.to_device(X["key"]), [cj.to_device(p) for p in X["payloads"]], "",
