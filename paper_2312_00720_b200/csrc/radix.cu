@@ -175,6 +175,9 @@ __global__ void __launch_bounds__(1024) k_digit_bases(const uint32_t* __restrict
   const uint32_t d = threadIdx.x % radix, q = threadIdx.x / radix;
   for (int p = 0; p < npasses; ++p) {
     uint64_t cq = 0;
+    // eight independent loads in flight per thread (a 1-CTA kernel: its time
+    // is the chain of load latencies, which dominates small joins)
+#pragma unroll 8
     for (uint32_t b = q; b < nblocks; b += split) cq += cnt[((uint64_t)b * npasses + p) * radix + d];
     part[threadIdx.x] = cq;
     __syncthreads();
@@ -432,6 +435,26 @@ __global__ void k_offsets(const K* __restrict__ keys, uint64_t n, uint32_t bits,
       if ((uint64_t)(keys[mid] & mask) < p) lo = mid + 1; else hi = mid;
     }
     off[p] = p == fanout ? n : lo;
+  }
+}
+
+// The same offsets by one pass over the keys: row i, the first row of its
+// digit, writes off[p] = i for every digit p between the previous row's digit
+// (exclusive) and its own; the last row fills the digits above it with n.
+// Reads n keys instead of (fanout + 1) binary searches of log2(n) dependent
+// loads: the faster one for small inputs (partition_offsets picks).
+template <class K>
+__global__ void k_offsets_scan(const K* __restrict__ keys, uint64_t n, uint32_t bits,
+                               uint64_t* __restrict__ off) {
+  const uint64_t fanout = 1ull << bits;
+  const K mask = (K)(fanout - 1);
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t d = (uint64_t)(keys[i] & mask);
+    const uint64_t prev = i ? (uint64_t)(keys[i - 1] & mask) + 1 : 0;  // first digit to set
+    for (uint64_t p = prev; p <= d; ++p) off[p] = i;
+    if (i == n - 1)
+      for (uint64_t p = d + 1; p <= fanout; ++p) off[p] = n;
   }
 }
 
@@ -1415,6 +1438,21 @@ PassPlan sort_plan(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes, con
 void partition_offsets(cj_ctx* ctx, const void* keys_sorted, uint64_t n, int key_bytes,
                        uint32_t bits, uint64_t* offsets_dev) {
   const uint64_t fanout = 1ull << bits;
+  // small inputs: one pass over the keys beats (fanout + 1) chains of
+  // log2(n) dependent loads (C1: 2^22 keys, 13 -> ~5 us)
+  if (n > 0 && n <= (1ull << 23)) {
+    ctx->kbegin("offsets", (uint64_t)key_bytes * n + 8 * (fanout + 1));
+    const unsigned g2 = grid_for(n, 256, ctx->num_sms * 8);
+    if (key_bytes == 4)
+      k_offsets_scan<uint32_t><<<g2, 256, 0, ctx->stream>>>(
+          static_cast<const uint32_t*>(keys_sorted), n, bits, offsets_dev);
+    else
+      k_offsets_scan<uint64_t><<<g2, 256, 0, ctx->stream>>>(
+          static_cast<const uint64_t*>(keys_sorted), n, bits, offsets_dev);
+    ctx->kend();
+    CJ_CUDA(cudaGetLastError());
+    return;
+  }
   const unsigned grid = grid_for(fanout + 1, 256, 4096);
   ctx->kbegin("offsets", 8 * (fanout + 1));
   if (key_bytes == 4)
