@@ -7,6 +7,8 @@ emission order for PHJ/SMJ, and as a row multiset for NPHJ (no reference
 counterpart) and for the sharded path at world 1.  Seeded, so a failure names
 a reproducible case.  (Round 2: found a speculation that ignored probe rows of
 partitions without build rows, and an undersized per-pass count scratch.)"""
+import os
+
 import numpy as np
 import pytest
 
@@ -36,6 +38,12 @@ def H(t):
     return cj.to_host(t).astype(np.uint64)
 
 
+# CJ_SWEEP_CASES / CJ_SWEEP_BASE widen or shift the join sweep for an ad hoc
+# longer run (default: the 100 committed seeds)
+N_CASES = int(os.environ.get("CJ_SWEEP_CASES", "100"))
+BASE = int(os.environ.get("CJ_SWEEP_BASE", "0"))
+
+
 def case(i):
     g = np.random.default_rng(1000 + i)
     kb = int(g.choice([4, 8]))
@@ -52,7 +60,7 @@ def case(i):
                 zipf=zipf, swap=swap, bits=bits, limit=limit)
 
 
-@pytest.mark.parametrize("i", range(100))
+@pytest.mark.parametrize("i", range(BASE, BASE + N_CASES))
 def test_random_case_matches_oracle(ctx, comm, i):
     c = case(i)
     R, S = O.gen_pk_fk(c["nr"], c["ns"], c["rpay"], c["spay"], match=c["match"], zipf=c["zipf"],
