@@ -155,9 +155,12 @@ ScatterGeom scatter_geom(cj_ctx* ctx, uint64_t n, int key_bytes, const ValCols& 
 
 // Per-block digit counts (cnt[b][p][256]) of every pass of `plan` (<= 8) in one
 // read of the keys, over the blocks of geometry g.
+// With totals_dev / base_dev, the last CTA also writes the digit totals and
+// exclusive bases of every pass (no separate launch).
 void block_hist(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes, const PassPlan& plan,
                 const ScatterGeom& g, uint32_t* cnt_dev, uint32_t hparts = 0,
-                uint32_t lowbits = 0, unsigned long long* key_or = nullptr);
+                uint32_t lowbits = 0, unsigned long long* key_or = nullptr,
+                uint32_t* totals_dev = nullptr, uint64_t* base_dev = nullptr);
 
 // block_hist + digit totals (totals_dev[p*256+d]) + exclusive digit bases
 // (base_dev[p*256+d]); totals_host after one host round trip when non-null.

@@ -47,7 +47,52 @@ struct HistArgs {
   uint32_t lowbits;  // shard mode: digit = shard << lowbits | low key bits
   uint32_t shift[8], mask[8];
   unsigned long long* key_or;  // optional: OR of every key (the join's dense-key test)
+  // optional: the last CTA to finish also writes the digit totals and
+  // exclusive bases of every pass (digit_bases_block; no launch of its own)
+  uint32_t* done;              // zeroed CTA ticket
+  uint32_t* totals;
+  uint64_t* base;
 };
+
+// Totals and exclusive digit bases per pass from the per-block counts
+// cnt[b][p][d], by one CTA (blockDim.x >= radix): thread (d, q) sums the
+// blocks b = q (mod split) of digit d (split = blockDim / radix independent
+// load streams), then threads q = 0 scan the digits.  part: blockDim words,
+// warp_tot: radix / 32 words of shared memory.
+__device__ __forceinline__ void digit_bases_block(const uint32_t* __restrict__ cnt, uint32_t nblocks,
+                                                  int npasses, uint32_t radix,
+                                                  uint32_t* __restrict__ totals,
+                                                  uint64_t* __restrict__ base, uint32_t* part,
+                                                  uint64_t* warp_tot) {
+  const uint32_t split = blockDim.x / radix;
+  const uint32_t d = threadIdx.x % radix, q = threadIdx.x / radix;
+  for (int p = 0; p < npasses; ++p) {
+    uint32_t cq = 0;
+    if (q < split) {
+      // eight independent loads in flight per thread (the chain of load
+      // latencies is this step's time)
+#pragma unroll 8
+      for (uint32_t b = q; b < nblocks; b += split)
+        cq += __ldcg(cnt + ((uint64_t)b * npasses + p) * radix + d);
+    }
+    part[threadIdx.x] = cq;
+    __syncthreads();
+    uint64_t c = 0, inc = 0;
+    if (q == 0) {
+      for (uint32_t i = 0; i < split; ++i) c += part[i * radix + d];
+      totals[p * radix + d] = (uint32_t)c;
+      inc = dev::warp_inclusive_sum(c);
+      if ((d & 31) == 31) warp_tot[d >> 5] = inc;
+    }
+    __syncthreads();
+    if (q == 0) {
+      uint64_t off = 0;
+      for (uint32_t w = 0; w < (d >> 5); ++w) off += warp_tot[w];
+      base[p * radix + d] = off + inc - c;
+    }
+    __syncthreads();
+  }
+}
 
 // Digit width: 8 bits (256 digits) everywhere, or 9 bits (512) for the
 // full-width sorts where it saves a pass (see lsd_partition).
@@ -135,6 +180,19 @@ k_block_hist(const K* __restrict__ keys, const __grid_constant__ HistArgs a,
     for (int w = 0; w < kCopies; ++w) t += sh[w * kWidth + d];
     if (t) atomicAdd(&cnt[b * kWidth + d], t);
   }
+  if (a.done) {  // the last CTA turns the counts into digit totals and bases
+    __shared__ bool s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(a.done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      // (the histogram copies are dead: their >= 4 KB hold part and warp_tot)
+      digit_bases_block(cnt, a.nblocks, NP, (uint32_t)kR, a.totals, a.base, sh,
+                        reinterpret_cast<uint64_t*>(sh + kHistThreads));
+    }
+  }
 }
 
 template <class K, int NP, bool SHARD, int RB>
@@ -158,43 +216,6 @@ void launch_hist_np(cj_ctx* ctx, const K* keys, const HistArgs& a, int np, uint3
     case 6: return launch_hist<K, 6, false, RB>(ctx, keys, a, cnt);
     case 7: return launch_hist<K, 7, false, RB>(ctx, keys, a, cnt);
     default: return launch_hist<K, 8, false, RB>(ctx, keys, a, cnt);
-  }
-}
-
-// Totals and exclusive digit bases per pass from the per-block counts.  One
-// block of 1024 threads: thread (d, q) sums the blocks b = q (mod split) of
-// digit d (split = 1024 / radix independent load streams instead of one
-// thread per digit walking every block), then threads q = 0 scan the digits.
-__global__ void __launch_bounds__(1024) k_digit_bases(const uint32_t* __restrict__ cnt,
-                                                      uint32_t nblocks, int npasses,
-                                                      uint32_t radix, uint32_t* __restrict__ totals,
-                                                      uint64_t* __restrict__ base) {
-  __shared__ uint64_t warp_tot[256 / 32];
-  __shared__ uint64_t part[1024];
-  const uint32_t split = blockDim.x / radix;
-  const uint32_t d = threadIdx.x % radix, q = threadIdx.x / radix;
-  for (int p = 0; p < npasses; ++p) {
-    uint64_t cq = 0;
-    // eight independent loads in flight per thread (a 1-CTA kernel: its time
-    // is the chain of load latencies, which dominates small joins)
-#pragma unroll 8
-    for (uint32_t b = q; b < nblocks; b += split) cq += cnt[((uint64_t)b * npasses + p) * radix + d];
-    part[threadIdx.x] = cq;
-    __syncthreads();
-    uint64_t c = 0, inc = 0;
-    if (q == 0) {
-      for (uint32_t i = 0; i < split; ++i) c += part[i * radix + d];
-      totals[p * radix + d] = (uint32_t)c;
-      inc = dev::warp_inclusive_sum(c);
-      if ((d & 31) == 31) warp_tot[d >> 5] = inc;
-    }
-    __syncthreads();
-    if (q == 0) {
-      uint64_t off = 0;
-      for (uint32_t w = 0; w < (d >> 5); ++w) off += warp_tot[w];
-      base[p * radix + d] = off + inc - c;
-    }
-    __syncthreads();
   }
 }
 
@@ -984,7 +1005,7 @@ ScatterGeom scatter_geom(cj_ctx* ctx, uint64_t n, int key_bytes, const ValCols& 
 
 void block_hist(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes, const PassPlan& plan,
                 const ScatterGeom& g, uint32_t* cnt_dev, uint32_t hparts, uint32_t lowbits,
-                unsigned long long* key_or) {
+                unsigned long long* key_or, uint32_t* totals_dev, uint64_t* base_dev) {
   const int np = plan.npasses;
   if (np < 1 || np > 8) fail(CJ_ERR_UNSUPPORTED, "histogram of 1..8 passes");
   HistArgs a{};
@@ -995,6 +1016,11 @@ void block_hist(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes, const 
   a.hparts = hparts;
   a.lowbits = lowbits;
   a.key_or = key_or;
+  if (totals_dev && base_dev) {
+    a.done = ctx->ticket(9);
+    a.totals = totals_dev;
+    a.base = base_dev;
+  }
   for (int p = 0; p < np; ++p) {
     a.shift[p] = plan.lo[p];
     a.mask[p] = (1u << (plan.hi[p] - plan.lo[p])) - 1u;
@@ -1025,12 +1051,10 @@ void histogram_passes(cj_ctx* ctx, const void* keys, uint64_t n, int key_bytes,
                       unsigned long long* key_or) {
   const int np = plan.npasses;
   if (np > 8) fail(CJ_ERR_UNSUPPORTED, "histogram of more than 8 passes");
-  block_hist(ctx, keys, n, key_bytes, plan, g, cnt_dev, hparts, lowbits, key_or);
+  // (the histogram's last CTA writes the totals and bases)
+  block_hist(ctx, keys, n, key_bytes, plan, g, cnt_dev, hparts, lowbits, key_or, totals_dev,
+             base_dev);
   const uint32_t R = 1u << g.rb;
-  ctx->kbegin("digit_bases", 12ull * R * np);
-  k_digit_bases<<<1, 1024, 0, ctx->stream>>>(cnt_dev, g.nblocks, np, R, totals_dev, base_dev);
-  ctx->kend();
-  CJ_CUDA(cudaGetLastError());
   if (totals_host) {
     totals_host->resize((size_t)R * np);
     CJ_CUDA(cudaMemcpyAsync(ctx->host_pinned, totals_dev, sizeof(uint32_t) * R * np,
@@ -1245,8 +1269,30 @@ void lsd_partition_group(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t
   // round trip for the digit totals; callers that know their passes are live
   // (ctx->assume_live_passes) run every pass instead and save the sync.
   const bool skip_check = ctx->assume_live_passes && !counts_out;
-  histogram_passes(ctx, keys, n, key_bytes, plan, g0, cnt.as<uint32_t>(), tot.as<uint32_t>(),
-                   base.as<uint64_t>(), skip_check ? nullptr : &totals, 0, 0, key_or);
+  // Four or more live passes (SMJ's 7-bit digits): counting every pass's
+  // digits in one read costs ~2x a read (four shared atomics per key), and the
+  // later passes re-read their keys for per-block counts anyway; so the first
+  // read counts only the first pass and each later pass takes its digit bases
+  // from its own re-read (the re-read's last CTA computes them).
+  int first_live = -1, nlive = 0;
+  for (int p = 0; p < np; ++p)
+    if (plan.hi[p] != plan.lo[p] && p >= plan.done) {
+      if (first_live < 0) first_live = p;
+      ++nlive;
+    }
+  const bool per_pass_bases = skip_check && nlive >= 4 && g0.tma;
+  if (per_pass_bases) {
+    PassPlan one;
+    one.npasses = 1;
+    one.lo[0] = plan.lo[first_live];
+    one.hi[0] = plan.hi[first_live];
+    histogram_passes(ctx, keys, n, key_bytes, one, g0, cnt.as<uint32_t>(),
+                     tot.as<uint32_t>() + (size_t)first_live * kRadix,
+                     base.as<uint64_t>() + (size_t)first_live * kRadix, nullptr, 0, 0, key_or);
+  } else {
+    histogram_passes(ctx, keys, n, key_bytes, plan, g0, cnt.as<uint32_t>(), tot.as<uint32_t>(),
+                     base.as<uint64_t>(), skip_check ? nullptr : &totals, 0, 0, key_or);
+  }
   if (counts_out) *counts_out = totals;
   std::vector<int> live;
   for (int p = 0; p < np; ++p) {
@@ -1293,20 +1339,27 @@ void lsd_partition_group(cj_ctx* ctx, const void* keys, void* keys_out, uint64_t
     // after an earlier pass (or a presorted first digit) the rows arrive in runs
     const int runs = li > 0 || plan.done > 0;
     if (li == 0) {
+      // (per_pass_bases: the first read counted this pass alone)
       scatter_pass(ctx, cur_k, tk, n, key_bytes, plan.lo[p], plan.hi[p], pbase,
-                   g0.tma ? cnt.as<uint32_t>() + (size_t)p * kRadix : nullptr,
-                   (uint32_t)(kRadix * np), g0, step, 0, 0, runs);
+                   g0.tma ? cnt.as<uint32_t>() + (per_pass_bases ? 0 : (size_t)p * kRadix) : nullptr,
+                   (uint32_t)(kRadix * (per_pass_bases ? 1 : np)), g0, step, 0, 0, runs);
     } else {
       const ScatterGeom g = scatter_geom(ctx, n, key_bytes, step, cur_k, rb);
       const uint32_t* pc = nullptr;
-      if (g.tma) {
+      if (g.tma || per_pass_bases) {
         PassPlan one;
         one.npasses = 1;
         one.lo[0] = plan.lo[p];
         one.hi[0] = plan.hi[p];
-        if ((uint64_t)g.nblocks > max_blocks) fail(CJ_ERR_CUDA, "block count scratch too small");
-        block_hist(ctx, cur_k, n, key_bytes, one, g, cnt2.as<uint32_t>());
-        pc = cnt2.as<uint32_t>();
+        // (a pass without the TMA geometry counts in the first pass's tiling:
+        // only its digit totals are used)
+        const ScatterGeom& gh = g.tma ? g : g0;
+        if ((uint64_t)gh.nblocks > max_blocks) fail(CJ_ERR_CUDA, "block count scratch too small");
+        // (per_pass_bases: its last CTA writes this pass's totals and bases)
+        block_hist(ctx, cur_k, n, key_bytes, one, gh, cnt2.as<uint32_t>(), 0, 0, nullptr,
+                   per_pass_bases ? tot.as<uint32_t>() + (size_t)p * kRadix : nullptr,
+                   per_pass_bases ? base.as<uint64_t>() + (size_t)p * kRadix : nullptr);
+        if (g.tma) pc = cnt2.as<uint32_t>();
       }
       scatter_pass(ctx, cur_k, tk, n, key_bytes, plan.lo[p], plan.hi[p], pbase, pc, kRadix, g,
                    step, 0, 0, runs);
