@@ -56,26 +56,30 @@ struct HistArgs {
 
 // Totals and exclusive digit bases per pass from the per-block counts
 // cnt[b][p][d], by one CTA (blockDim.x >= radix): thread (d, q) sums the
-// blocks b = q (mod split) of digit d (split = blockDim / radix independent
-// load streams), then threads q = 0 scan the digits.  part: blockDim words,
+// blocks b = q (mod split) of digit d for every pass at once (split =
+// blockDim / radix independent load streams, NP loads per block in flight),
+// then threads q = 0 scan the digits pass by pass.  part: blockDim words,
 // warp_tot: radix / 32 words of shared memory.
+template <int NP>
 __device__ __forceinline__ void digit_bases_block(const uint32_t* __restrict__ cnt, uint32_t nblocks,
-                                                  int npasses, uint32_t radix,
-                                                  uint32_t* __restrict__ totals,
+                                                  uint32_t radix, uint32_t* __restrict__ totals,
                                                   uint64_t* __restrict__ base, uint32_t* part,
                                                   uint64_t* warp_tot) {
   const uint32_t split = blockDim.x / radix;
   const uint32_t d = threadIdx.x % radix, q = threadIdx.x / radix;
-  for (int p = 0; p < npasses; ++p) {
-    uint32_t cq = 0;
-    if (q < split) {
-      // eight independent loads in flight per thread (the chain of load
-      // latencies is this step's time)
-#pragma unroll 8
-      for (uint32_t b = q; b < nblocks; b += split)
-        cq += __ldcg(cnt + ((uint64_t)b * npasses + p) * radix + d);
+  uint32_t cq[NP];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) cq[p] = 0;
+  if (q < split) {
+#pragma unroll 4
+    for (uint32_t b = q; b < nblocks; b += split) {
+#pragma unroll
+      for (int p = 0; p < NP; ++p) cq[p] += __ldcg(cnt + ((uint64_t)b * NP + p) * radix + d);
     }
-    part[threadIdx.x] = cq;
+  }
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    part[threadIdx.x] = cq[p];
     __syncthreads();
     uint64_t c = 0, inc = 0;
     if (q == 0) {
@@ -189,8 +193,8 @@ k_block_hist(const K* __restrict__ keys, const __grid_constant__ HistArgs a,
     if (s_last) {
       __threadfence();
       // (the histogram copies are dead: their >= 4 KB hold part and warp_tot)
-      digit_bases_block(cnt, a.nblocks, NP, (uint32_t)kR, a.totals, a.base, sh,
-                        reinterpret_cast<uint64_t*>(sh + kHistThreads));
+      digit_bases_block<NP>(cnt, a.nblocks, (uint32_t)kR, a.totals, a.base, sh,
+                            reinterpret_cast<uint64_t*>(sh + kHistThreads));
     }
   }
 }
