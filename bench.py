@@ -160,6 +160,7 @@ class Clocks:
          "clocks_event_reasons.sw_power_cap,power.draw")
 
     def __init__(self, gpu: int):
+        self.gpu = gpu
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu), f"--query-gpu={self.Q}",
@@ -175,15 +176,30 @@ class Clocks:
         self.p.wait()
         self.f.seek(0)
         rows = [r.split(", ") for r in self.f.read().strip().splitlines() if r.strip()]
+        note = None
+        if not rows:
+            # a timed region shorter than nvidia-smi's start-up (C1): one
+            # sample right after it, while the clocks still reflect the load
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=30).stdout
+                rows = [r.split(", ") for r in out.strip().splitlines() if r.strip()]
+                note = "timed region shorter than the sampler's start-up: one sample right after it"
+            except Exception:
+                rows = []
         sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in rows for i in range(4)
                           if len(r) > 2 + i and r[2 + i].strip() == "Active"})
         busy = [x for x in sm if x > 600] or sm
-        return {"sm_mhz": statistics.median(busy) if busy else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(rows)}
+        out = {"sm_mhz": statistics.median(busy) if busy else None,
+               "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+               "samples": len(rows)}
+        if note:
+            out["note"] = note
+        return out
 
 
 def config_dict(cfg, a, nr, ns, world):
